@@ -1,0 +1,119 @@
+/* ringcp_b200 — C ABI of the B200-native context-parallel attention engine.
+ *
+ * Drop-in boundary for the reference package `ringcp` (arXiv 2411.01783,
+ * /root/reference/pkg/src/ringcp).  The reference is a Python API; every entry
+ * point below is what that API's hot path calls on a B200, one call per
+ * reference operation (file:line of the operation it replaces is given).
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers unless stated; nothing here allocates or
+ *     frees caller memory.  Every call is asynchronous on `stream`
+ *     (a cudaStream_t passed as void*), stream-ordered, and returns
+ *     RCP_OK (0) or a negative error class; rcp_last_error() returns the
+ *     thread-local message of the last failure.
+ *   - Token-major layouts, bf16 inputs:  Q [Tq, Hq, 128], K/V [Tk, Hkv, 128]
+ *     with an explicit row stride (elements between consecutive tokens,
+ *     multiple of 8).  Outputs are fp32: O [Tq, Hq, 128] (contiguous) and
+ *     LSE [Tq, Hq] (natural log, -inf for rows that admitted no key).
+ *   - Per-token metadata is int32 and already FOLDED with the validity bit:
+ *       valid query  : pos >= 0,  seq = its sequence id
+ *       padding query: pos = -1,  seq = RCP_SEQ_PAD_Q   (INT32_MIN)
+ *       valid key    : pos >= 0,  seq = its sequence id
+ *       padding key  : pos = INT32_MAX, seq = RCP_SEQ_PAD_K (INT32_MIN + 1)
+ *     so key j is admitted for query i iff seq_k[j] == seq_q[i] and
+ *     pos_k[j] <= pos_q[i]  (ringcp.attention._admissible, attention.py:199-206).
+ */
+#ifndef RINGCP_B200_H
+#define RINGCP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RCP_OK 0
+#define RCP_ERR_INVALID (-1)   /* bad argument: shape/alignment/geometry      */
+#define RCP_ERR_CUDA (-2)      /* CUDA runtime/driver failure                 */
+#define RCP_ERR_UNSUPPORTED (-3)
+
+#define RCP_SEQ_PAD_Q (-2147483647 - 1)
+#define RCP_SEQ_PAD_K (-2147483647)
+#define RCP_POS_PAD_K 2147483647
+
+#define RCP_MODE_OVERWRITE 0  /* O, LSE <- attention of this KV block                 */
+#define RCP_MODE_MERGE 1      /* (O, LSE) <- merge((O, LSE), attention of this block) */
+
+const char* rcp_last_error(void);
+const char* rcp_version(void);
+
+/* Workspace bytes rcp_attn_fwd needs for a (Tq, Tk) call (tile summaries). */
+size_t rcp_attn_workspace_bytes(int64_t tq, int64_t tk);
+
+/* Causal-by-position GQA attention of one query block against one KV block,
+ * with per-row LSE.  Replaces ringcp.attention.gqa_attention
+ * (attention.py:230-282).  head_dim must be 128; hq % hkv == 0; query head h
+ * reads kv head h / (hq / hkv) (GqaConfig.query_to_kv_head, attention.py:64-66).
+ * mode RCP_MODE_MERGE folds the result into (o, lse) with the pairwise merge of
+ * ringcp.attention._merge_pair (attention.py:299-316) — the running merge of
+ * the pass-KV ring (Alg. 2).  Padding key rows must hold
+ * finite data (the Python layer zeroes them). */
+int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k, int64_t k_row_stride,
+                 const void* v, int64_t v_row_stride, const int32_t* q_pos,
+                 const int32_t* q_seq, const int32_t* k_pos, const int32_t* k_seq, int64_t tq,
+                 int64_t tk, int32_t hq, int32_t hkv, int32_t head_dim, float scale, float* o,
+                 float* lse, int32_t mode, void* workspace, size_t workspace_bytes,
+                 void* stream);
+
+/* Left-fold merge of n partials (ascending list order), replacing
+ * ringcp.attention.merge_attention (attention.py:319-334).  o_parts / lse_parts
+ * are HOST arrays of n DEVICE pointers, each O [rows, head_dim] fp32 and LSE
+ * [rows] fp32 (rows = Tq * Hq, head_dim % 4 == 0).  Output may alias part 0. */
+int rcp_merge_attn(const float* const* o_parts, const float* const* lse_parts, int32_t n,
+                   int64_t rows, int32_t head_dim, float* o_out, float* lse_out, void* stream);
+
+/* Fill O = 0 and LSE = -inf (the result of attending to no key). */
+int rcp_fill_empty(float* o, float* lse, int64_t rows, int32_t head_dim, void* stream);
+
+/* Load-balanced shard gather: the device half of
+ * ringcp.sharding.materialize_rank_block (sharding.py:211-240).
+ * For each of n_seqs sequences (HOST arrays, one entry per sequence):
+ *   src_rows[i]   device pointer to sequence i's dense new-token rows
+ *   new_len[i], cached_len[i], seq_id[i]
+ * writes dst (n_seqs * 2 * chunk_len_i slots, row_bytes each) with rank
+ * `rank`'s chunks (C_rank, C_{2N-1-rank}), zero padding, and (optionally, if
+ * non-null) the folded metadata pos/seq (query or key sentinels per
+ * `is_key`) — positions = cached_len + local index (sharding.py:235). */
+int rcp_shard_gather(void* dst, const void* const* src_rows, const int64_t* new_len,
+                     const int64_t* cached_len, const int64_t* seq_id, int32_t n_seqs,
+                     int32_t n_ranks, int32_t rank, int64_t row_bytes, int32_t* pos_out,
+                     int32_t* seq_out, int32_t is_key, void* stream);
+
+/* Row gather dst[i] = src[idx[i]] (idx < 0 -> zero row), idx int64 on device. */
+int rcp_gather_rows(void* dst, const void* src, const int64_t* idx, int64_t n_rows,
+                    int64_t row_bytes, void* stream);
+
+/* Fold int64 positions / seq ids / bool valid into the int32 kernel metadata
+ * described above.  is_key selects the key sentinels. */
+int rcp_fold_meta(const int64_t* pos, const int64_t* seq, const uint8_t* valid, int64_t n,
+                  int32_t is_key, int32_t* pos_out, int32_t* seq_out, void* stream);
+
+/* Split-KV decode attention: one query token per sequence against the rank's
+ * cached KV shard of that sequence (ring pass-Q decode, Alg. 4,
+ * PAPER.md:353-370).  q [B, hq, 128] bf16; for sequence b the keys are rows
+ * [kv_start[b], kv_start[b] + kv_len[b]) of k/v ([rows, hkv, 128] bf16,
+ * row stride kv_row_stride), all causally visible (cache holds only the
+ * past and the token itself) and same-sequence.  kv_start/kv_len are device
+ * int64 arrays.  Writes o [B, hq, 128] fp32, lse [B, hq] fp32 (-inf when
+ * kv_len == 0).  workspace: rcp_decode_workspace_bytes(B, hq, max_len). */
+size_t rcp_decode_workspace_bytes(int64_t batch, int32_t hq, int64_t max_kv_len);
+int rcp_decode_attn(const void* q, const void* k, const void* v, int64_t kv_row_stride,
+                    const int64_t* kv_start, const int64_t* kv_len, int64_t batch,
+                    int64_t max_kv_len, int32_t hq, int32_t hkv, int32_t head_dim, float scale,
+                    float* o, float* lse, void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RINGCP_B200_H */

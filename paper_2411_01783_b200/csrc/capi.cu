@@ -1,0 +1,322 @@
+// C-ABI plumbing and the HBM-bound helper kernels of ringcp-b200:
+// error state, tile summaries, metadata folding, the N-way LSE merge (K2),
+// the empty-result fill and the row gathers behind materialize_rank_block (K0).
+#include <climits>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace rcp {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+// ------------------------------------------------------------------ tile summary
+__global__ void __launch_bounds__(128) tile_summary_kernel(const int32_t* __restrict__ pos,
+                                                           const int32_t* __restrict__ seq,
+                                                           int64_t n, int32_t pad_seq,
+                                                           TileSum* __restrict__ out) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 128 + threadIdx.x;
+  int p = 0, s = 0;
+  bool valid = false;
+  if (row < n) {
+    s = seq[row];
+    p = pos[row];
+    valid = (s != pad_seq);
+  }
+  int pmin = valid ? p : INT_MAX, pmax = valid ? p : INT_MIN;
+  int smin = valid ? s : INT_MAX, smax = valid ? s : INT_MIN;
+  int cnt = valid ? 1 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    pmin = min(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
+    pmax = max(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+    smin = min(smin, __shfl_xor_sync(0xffffffffu, smin, o));
+    smax = max(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  __shared__ int red[4][5];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[w][0] = pmin;
+    red[w][1] = pmax;
+    red[w][2] = smin;
+    red[w][3] = smax;
+    red[w][4] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    TileSum t;
+    t.pmin = min(min(red[0][0], red[1][0]), min(red[2][0], red[3][0]));
+    t.pmax = max(max(red[0][1], red[1][1]), max(red[2][1], red[3][1]));
+    t.smin = min(min(red[0][2], red[1][2]), min(red[2][2], red[3][2]));
+    t.smax = max(max(red[0][3], red[1][3]), max(red[2][3], red[3][3]));
+    t.nvalid = red[0][4] + red[1][4] + red[2][4] + red[3][4];
+    t.uniform = (t.nvalid == 128 && t.smin == t.smax) ? 1 : 0;
+    t.pad0 = t.pad1 = 0;
+    out[blockIdx.x] = t;
+  }
+}
+
+int launch_tile_summary(const int32_t* pos, const int32_t* seq, int64_t n, int32_t pad_seq,
+                        TileSum* out, cudaStream_t stream) {
+  const int64_t tiles = (n + 127) / 128;
+  if (tiles == 0) return RCP_OK;
+  tile_summary_kernel<<<static_cast<unsigned>(tiles), 128, 0, stream>>>(pos, seq, n, pad_seq,
+                                                                         out);
+  RCP_CUDA(cudaGetLastError());
+  return RCP_OK;
+}
+
+// ------------------------------------------------------------------ metadata fold
+__global__ void fold_meta_kernel(const int64_t* __restrict__ pos, const int64_t* __restrict__ seq,
+                                 const uint8_t* __restrict__ valid, int64_t n, int32_t is_key,
+                                 int32_t* __restrict__ pos_out, int32_t* __restrict__ seq_out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const bool ok = valid[i] != 0;
+    if (ok) {
+      pos_out[i] = static_cast<int32_t>(pos[i]);
+      seq_out[i] = static_cast<int32_t>(seq[i]);
+    } else {
+      pos_out[i] = is_key ? RCP_POS_PAD_K : -1;
+      seq_out[i] = is_key ? RCP_SEQ_PAD_K : RCP_SEQ_PAD_Q;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ fill / merge
+__global__ void fill_empty_kernel(float4* __restrict__ o, float* __restrict__ lse, int64_t rows) {
+  const int64_t n4 = rows * 32;  // 128 floats per row
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    o[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if ((i & 31) == 0) lse[i >> 5] = -INFINITY;
+  }
+}
+
+constexpr int kMaxMergeParts = 64;
+struct MergeArgs {
+  const float* o[kMaxMergeParts];
+  const float* lse[kMaxMergeParts];
+};
+
+// One warp per (token, head) row of D values (D % 4 == 0), float4 per lane.
+// Left fold over parts in list order — merge_attention (attention.py:319-334).
+__global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ MergeArgs a,
+                                                    int32_t n, int64_t rows, int32_t d4,
+                                                    float* __restrict__ o_out,
+                                                    float* __restrict__ lse_out) {
+  const int64_t row = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  float la_final = 0.f;
+  for (int c = lane; c < d4; c += 32) {
+    float4 acc = __ldg(reinterpret_cast<const float4*>(a.o[0] + row * d4 * 4) + c);
+    float la = __ldg(a.lse[0] + row);
+    for (int s = 1; s < n; ++s) {
+      const float4 b = __ldg(reinterpret_cast<const float4*>(a.o[s] + row * d4 * 4) + c);
+      const float lb = __ldg(a.lse[s] + row);
+      const MergeW w = merge_weights(la, lb);
+      acc.x = merge_val(acc.x, b.x, w);
+      acc.y = merge_val(acc.y, b.y, w);
+      acc.z = merge_val(acc.z, b.z, w);
+      acc.w = merge_val(acc.w, b.w, w);
+      la = w.lse;
+    }
+    reinterpret_cast<float4*>(o_out + row * d4 * 4)[c] = acc;
+    la_final = la;
+  }
+  if (lane == 0) lse_out[row] = la_final;
+}
+
+// ------------------------------------------------------------------ gathers
+// Generic row gather, one warp per row, 16-byte vectors:
+// dst[i] = idx[i] >= 0 ? src[idx[i]] : 0.
+__global__ void gather_rows_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                   const int64_t* __restrict__ idx, int64_t n_rows,
+                                   int64_t vec_per_row) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+       r < n_rows; r += warps) {
+    const int64_t s = idx[r];
+    uint4* d = dst + r * vec_per_row;
+    if (s >= 0) {
+      const uint4* sp = src + s * vec_per_row;
+      for (int64_t c = lane; c < vec_per_row; c += 32) d[c] = __ldg(sp + c);
+    } else {
+      for (int64_t c = lane; c < vec_per_row; c += 32) d[c] = make_uint4(0, 0, 0, 0);
+    }
+  }
+}
+
+constexpr int kMaxShardSeqs = 64;
+struct ShardArgs {
+  const uint4* src[kMaxShardSeqs];
+  int64_t slot_begin[kMaxShardSeqs + 1];  // first dst slot of each sequence
+  int64_t chunk[kMaxShardSeqs];           // chunk_len = ceil(T / 2N)
+  int64_t new_len[kMaxShardSeqs];
+  int64_t cached[kMaxShardSeqs];
+  int64_t seq_id[kMaxShardSeqs];
+};
+
+// materialize_rank_block on device (sharding.py:105-115, 211-240): slot s of
+// sequence i holds local token lo*c + s (s < c) or hi*c + (s - c), where
+// (lo, hi) = (rank, 2N-1-rank); local indices >= new_len are padding.
+// One warp per destination slot; lanes stream the row in 16-byte vectors.
+__global__ void shard_gather_kernel(const __grid_constant__ ShardArgs a, int32_t n_seqs,
+                                    int32_t n_ranks, int32_t rank, int64_t vec_per_row,
+                                    uint4* __restrict__ dst, int32_t* __restrict__ pos_out,
+                                    int32_t* __restrict__ seq_out, int32_t is_key) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total_slots = a.slot_begin[n_seqs];
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t slot = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+       slot < total_slots; slot += warps) {
+    int sq = 0;
+    while (sq + 1 < n_seqs && a.slot_begin[sq + 1] <= slot) ++sq;
+    const int64_t s = slot - a.slot_begin[sq];
+    const int64_t ch = a.chunk[sq];
+    const int64_t chunk_id = s < ch ? rank : 2 * n_ranks - 1 - rank;
+    const int64_t local = chunk_id * ch + (s < ch ? s : s - ch);
+    const bool valid = local < a.new_len[sq];
+    uint4* d = dst + slot * vec_per_row;
+    if (valid) {
+      const uint4* sp = a.src[sq] + local * vec_per_row;
+      for (int64_t c = lane; c < vec_per_row; c += 32) d[c] = __ldg(sp + c);
+    } else {
+      for (int64_t c = lane; c < vec_per_row; c += 32) d[c] = make_uint4(0, 0, 0, 0);
+    }
+    if (lane == 0 && pos_out != nullptr) {
+      pos_out[slot] = valid ? static_cast<int32_t>(a.cached[sq] + local)
+                            : (is_key ? RCP_POS_PAD_K : -1);
+      seq_out[slot] = valid ? static_cast<int32_t>(a.seq_id[sq])
+                            : (is_key ? RCP_SEQ_PAD_K : RCP_SEQ_PAD_Q);
+    }
+  }
+}
+
+static unsigned grid_for(int64_t work, int threads) {
+  int64_t b = (work + threads - 1) / threads;
+  const int64_t cap = 148 * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return static_cast<unsigned>(b);
+}
+
+}  // namespace rcp
+
+using namespace rcp;
+
+extern "C" {
+
+const char* rcp_last_error(void) { return g_last_error.c_str(); }
+
+const char* rcp_version(void) { return "ringcp_b200 0.1.0 sm_100a"; }
+
+int rcp_fold_meta(const int64_t* pos, const int64_t* seq, const uint8_t* valid, int64_t n,
+                  int32_t is_key, int32_t* pos_out, int32_t* seq_out, void* stream) {
+  RCP_CHECK_ARG(n >= 0, "n must be >= 0");
+  if (n == 0) return RCP_OK;
+  RCP_CHECK_ARG(pos && seq && valid && pos_out && seq_out, "null pointer");
+  fold_meta_kernel<<<grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      pos, seq, valid, n, is_key, pos_out, seq_out);
+  RCP_CUDA(cudaGetLastError());
+  return RCP_OK;
+}
+
+int rcp_fill_empty(float* o, float* lse, int64_t rows, int32_t head_dim, void* stream) {
+  RCP_CHECK_ARG(head_dim == 128, "head_dim must be 128, got %d", head_dim);
+  RCP_CHECK_ARG(rows >= 0, "rows must be >= 0");
+  if (rows == 0) return RCP_OK;
+  RCP_CHECK_ARG((reinterpret_cast<uintptr_t>(o) & 15) == 0, "o must be 16-byte aligned");
+  fill_empty_kernel<<<grid_for(rows * 32, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<float4*>(o), lse, rows);
+  RCP_CUDA(cudaGetLastError());
+  return RCP_OK;
+}
+
+int rcp_merge_attn(const float* const* o_parts, const float* const* lse_parts, int32_t n,
+                   int64_t rows, int32_t head_dim, float* o_out, float* lse_out, void* stream) {
+  RCP_CHECK_ARG(n >= 1, "cannot merge an empty list of partials");
+  RCP_CHECK_ARG(n <= kMaxMergeParts, "at most %d partials per merge call", kMaxMergeParts);
+  RCP_CHECK_ARG(head_dim >= 4 && head_dim % 4 == 0, "head_dim must be a positive multiple of 4");
+  RCP_CHECK_ARG(rows >= 0, "rows must be >= 0");
+  if (rows == 0) return RCP_OK;
+  MergeArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int i = 0; i < n; ++i) {
+    RCP_CHECK_ARG(o_parts[i] && lse_parts[i], "null partial %d", i);
+    RCP_CHECK_ARG((reinterpret_cast<uintptr_t>(o_parts[i]) & 15) == 0,
+                  "partial %d output must be 16-byte aligned", i);
+    a.o[i] = o_parts[i];
+    a.lse[i] = lse_parts[i];
+  }
+  const int64_t threads = rows * 32;
+  const unsigned blocks = static_cast<unsigned>((threads + 255) / 256);
+  merge_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, n, rows, head_dim / 4, o_out,
+                                                                   lse_out);
+  RCP_CUDA(cudaGetLastError());
+  return RCP_OK;
+}
+
+int rcp_gather_rows(void* dst, const void* src, const int64_t* idx, int64_t n_rows,
+                    int64_t row_bytes, void* stream) {
+  RCP_CHECK_ARG(n_rows >= 0 && row_bytes > 0, "bad sizes");
+  RCP_CHECK_ARG(row_bytes % 16 == 0, "row_bytes must be a multiple of 16");
+  RCP_CHECK_ARG((reinterpret_cast<uintptr_t>(dst) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(src) & 15) == 0,
+                "dst/src must be 16-byte aligned");
+  if (n_rows == 0) return RCP_OK;
+  const int64_t vpr = row_bytes / 16;
+  gather_rows_kernel<<<grid_for(n_rows * 32, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<uint4*>(dst), static_cast<const uint4*>(src), idx, n_rows, vpr);
+  RCP_CUDA(cudaGetLastError());
+  return RCP_OK;
+}
+
+int rcp_shard_gather(void* dst, const void* const* src_rows, const int64_t* new_len,
+                     const int64_t* cached_len, const int64_t* seq_id, int32_t n_seqs,
+                     int32_t n_ranks, int32_t rank, int64_t row_bytes, int32_t* pos_out,
+                     int32_t* seq_out, int32_t is_key, void* stream) {
+  RCP_CHECK_ARG(n_ranks >= 1, "n_ranks must be >= 1");
+  RCP_CHECK_ARG(rank >= 0 && rank < n_ranks, "rank %d out of range for %d ranks", rank, n_ranks);
+  RCP_CHECK_ARG(n_seqs >= 1, "cannot plan an empty sequence list");
+  RCP_CHECK_ARG(n_seqs <= kMaxShardSeqs, "at most %d sequences per gather", kMaxShardSeqs);
+  RCP_CHECK_ARG(row_bytes > 0 && row_bytes % 16 == 0, "row_bytes must be a positive multiple of 16");
+  RCP_CHECK_ARG((reinterpret_cast<uintptr_t>(dst) & 15) == 0, "dst must be 16-byte aligned");
+  ShardArgs a;
+  memset(&a, 0, sizeof(a));
+  int64_t slot = 0;
+  for (int i = 0; i < n_seqs; ++i) {
+    RCP_CHECK_ARG(new_len[i] >= 1, "sequence %lld has no new tokens", (long long)seq_id[i]);
+    RCP_CHECK_ARG((reinterpret_cast<uintptr_t>(src_rows[i]) & 15) == 0,
+                  "source of sequence %d must be 16-byte aligned", i);
+    RCP_CHECK_ARG(cached_len[i] + new_len[i] <= INT32_MAX, "positions exceed int32");
+    a.src[i] = static_cast<const uint4*>(src_rows[i]);
+    a.chunk[i] = (new_len[i] + 2 * n_ranks - 1) / (2 * n_ranks);
+    a.new_len[i] = new_len[i];
+    a.cached[i] = cached_len[i];
+    a.seq_id[i] = seq_id[i];
+    a.slot_begin[i] = slot;
+    slot += 2 * a.chunk[i];
+  }
+  a.slot_begin[n_seqs] = slot;
+  const int64_t vpr = row_bytes / 16;
+  shard_gather_kernel<<<grid_for(slot * 32, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      a, n_seqs, n_ranks, rank, vpr, static_cast<uint4*>(dst), pos_out, seq_out, is_key);
+  RCP_CUDA(cudaGetLastError());
+  return RCP_OK;
+}
+
+}  // extern "C"

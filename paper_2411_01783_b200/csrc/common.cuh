@@ -1,0 +1,87 @@
+// Shared host/device pieces of the ringcp-b200 C ABI: error reporting, the
+// fp32 LSE merge used by both the fused attention epilogue and the merge
+// kernel (so pass-KV and pass-Q fold bit-identically), and tile summaries.
+#pragma once
+
+#include <cstdarg>
+#include <cstdio>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "ringcp_b200.h"
+
+namespace rcp {
+
+// ------------------------------------------------------------------ errors
+void set_error(const char* fmt, ...);
+
+#define RCP_CHECK_ARG(cond, ...)      \
+  do {                                \
+    if (!(cond)) {                    \
+      ::rcp::set_error(__VA_ARGS__);  \
+      return RCP_ERR_INVALID;         \
+    }                                 \
+  } while (0)
+
+#define RCP_CUDA(call)                                                              \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      ::rcp::set_error("%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                       __LINE__);                                                   \
+      return RCP_ERR_CUDA;                                                          \
+    }                                                                               \
+  } while (0)
+
+// ------------------------------------------------------------------ merge math
+// One pairwise LSE merge step, the fp32 restatement of
+// ringcp.attention._merge_pair (attention.py:299-316).  Written with explicit
+// round-to-nearest intrinsics so every kernel that folds partials produces the
+// same bits regardless of FMA contraction.
+struct MergeW {
+  float lse, wa, wb;
+};
+__device__ __forceinline__ MergeW merge_weights(float la, float lb) {
+  const float m = fmaxf(la, lb);
+  MergeW r;
+  if (m == -INFINITY) {
+    r.lse = -INFINITY;
+    r.wa = 0.f;
+    r.wb = 0.f;
+    return r;
+  }
+  const float tot = __fadd_rn(expf(__fsub_rn(la, m)), expf(__fsub_rn(lb, m)));
+  r.lse = __fadd_rn(m, logf(tot));
+  r.wa = (la == -INFINITY) ? 0.f : expf(__fsub_rn(la, r.lse));
+  r.wb = (lb == -INFINITY) ? 0.f : expf(__fsub_rn(lb, r.lse));
+  return r;
+}
+__device__ __forceinline__ float merge_val(float a, float b, const MergeW& w) {
+  return __fadd_rn(__fmul_rn(a, w.wa), __fmul_rn(b, w.wb));
+}
+
+// ------------------------------------------------------------------ tile summaries
+// Per 128-token tile of a block: min/max position and sequence id over the
+// VALID rows, number of valid rows, and whether all 128 rows are valid and of
+// one sequence.  Used to classify (query tile, key tile) pairs as empty / full
+// / partial so masked work is skipped and unmasked tiles skip the mask.
+struct __align__(32) TileSum {
+  int pmin, pmax, smin, smax, nvalid, uniform, pad0, pad1;
+};
+
+enum : int { kTileEmpty = 0, kTilePartial = 1, kTileFull = 2 };
+
+__host__ __device__ __forceinline__ int classify_tile(const TileSum& q, const TileSum& k) {
+  if (q.nvalid == 0 || k.nvalid == 0) return kTileEmpty;
+  if (k.pmin > q.pmax) return kTileEmpty;
+  if (k.smax < q.smin || k.smin > q.smax) return kTileEmpty;
+  if (q.uniform && k.uniform && q.smin == k.smin && k.pmax <= q.pmin) return kTileFull;
+  return kTilePartial;
+}
+
+// Launch the summary kernel for one metadata array (n rows, 128-row tiles).
+int launch_tile_summary(const int32_t* pos, const int32_t* seq, int64_t n, int32_t pad_seq,
+                        TileSum* out, cudaStream_t stream);
+
+}  // namespace rcp
