@@ -249,7 +249,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       mbar_wait(&bar_s[w], it & 1);
       tc_fence_after();
       uint32_t pk[64];
-      bool any_p = false;
       if (cls != kTileEmpty) {
         uint32_t sr[128];
 #pragma unroll
@@ -288,35 +287,35 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         const float m_new = fmaxf(m, mx * sl2);
         const bool need = m_new > m + kRescaleThreshold;  // also true for -inf -> finite
         if (need) m = m_new;
-        if (m != -INFINITY) {
-          any_p = true;
-          float sum = 0.f;
+        // Rows that have admitted nothing yet keep m = -inf: their scores are all
+        // -inf, so exp2(s - 0) = 0.  Everything below is warp-uniform (the
+        // tcgen05.ld/st are .sync.aligned).
+        const float m_use = (m == -INFINITY) ? 0.f : m;
+        float sum = 0.f;
 #pragma unroll
-          for (int c = 0; c < 128; c += 2) {
-            const float p0 = ex2_approx(fmaf(s[c], sl2, -m));
-            const float p1 = ex2_approx(fmaf(s[c + 1], sl2, -m));
-            sum += p0 + p1;
-            pk[c >> 1] = pack_bf16x2(p0, p1);
-          }
-          const float f = (need && m_old != -INFINITY) ? ex2_approx(m_old - m) : 1.0f;
-          l = (m_old == -INFINITY ? 0.f : l * f) + sum;
-          tmem_st32(s_addr, pk);
-          tmem_st32(s_addr + 32, pk + 32);
-          if (__any_sync(0xffffffffu, f != 1.0f && it > 0)) {
-            // Rescale O_t rows in place (TMEM); PV_t(it-1) is complete (see header).
+        for (int c = 0; c < 128; c += 2) {
+          const float p0 = ex2_approx(fmaf(s[c], sl2, -m_use));
+          const float p1 = ex2_approx(fmaf(s[c + 1], sl2, -m_use));
+          sum += p0 + p1;
+          pk[c >> 1] = pack_bf16x2(p0, p1);
+        }
+        const float f = (need && m_old != -INFINITY) ? ex2_approx(m_old - m) : 1.0f;
+        l = (m_old == -INFINITY ? 0.f : l * f) + sum;
+        tmem_st32(s_addr, pk);
+        tmem_st32(s_addr + 32, pk + 32);
+        if (__any_sync(0xffffffffu, f != 1.0f && it > 0)) {
+          // Rescale O_t rows in place (TMEM); PV_t(it-1) is complete (see header).
 #pragma unroll
-            for (int c = 0; c < 128; c += 32) {
-              uint32_t r[32];
-              tmem_ld32(o_addr + c, r);
-              tmem_ld_wait();
+          for (int c = 0; c < 128; c += 32) {
+            uint32_t r[32];
+            tmem_ld32(o_addr + c, r);
+            tmem_ld_wait();
 #pragma unroll
-              for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
-              tmem_st32(o_addr + c, r);
-            }
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
+            tmem_st32(o_addr + c, r);
           }
         }
-      }
-      if (!any_p) {
+      } else {
 #pragma unroll
         for (int i = 0; i < 64; ++i) pk[i] = 0u;
         tmem_st32(s_addr, pk);

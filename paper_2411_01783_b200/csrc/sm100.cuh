@@ -65,10 +65,24 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar_addr, uint32_t parity
       : "memory");
   return ok != 0;
 }
+// Spin on an mbarrier phase.  With RCP_WATCHDOG (default on) a wait that
+// exceeds ~2^33 SM cycles traps, turning a pipeline deadlock into a launch
+// error instead of a hung GPU.
+#ifndef RCP_WATCHDOG
+#define RCP_WATCHDOG 1
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
+  if (mbar_try_wait(a, parity)) return;
+#if RCP_WATCHDOG
+  const long long t0 = clock64();
+  while (!mbar_try_wait(a, parity)) {
+    if (clock64() - t0 > (1ll << 33)) __trap();
+  }
+#else
   while (!mbar_try_wait(a, parity)) {
   }
+#endif
 }
 
 // ---------------------------------------------------------------- TMA

@@ -1,0 +1,183 @@
+"""Per-rank persistent KV store on the GPU — the SPEC's ``RankKvCache``.
+
+Reference: SPEC.md:167-219 (module ``kv_cache``; not shipped in pkg/).  One
+cache per rank holds, for every sequence, only VALID key/value rows in
+ascending position order.  Storage is one HBM arena per rank
+(K, V as [capacity, n_kv_heads, head_dim] bf16 plus folded int32 key
+metadata), each sequence owning a contiguous segment that grows by doubling,
+so decode appends are O(1) and a sequence's history is a single contiguous
+row range — exactly what the decode kernel (rcp_decode_attn) and the ring
+message builder need.
+
+Position bookkeeping lives on the host (every append comes from a plan whose
+positions the host knows, or is checked once), so snapshots and ring messages
+are built without device synchronisation.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .attention import EmbeddingBlock, _device
+
+__all__ = ["RankKvCache"]
+
+
+@dataclass
+class _Segment:
+    start: int      # first arena row
+    cap: int        # rows reserved
+    length: int     # rows used
+    max_pos: int    # largest cached position (-1 when empty)
+
+
+class RankKvCache:
+    """``append(seq_id, k_block, v_block) -> cached_len`` and
+    ``snapshot_padded(seq_id, max_len) -> (k_block, v_block)`` as in SPEC.md:180-198."""
+
+    def __init__(self, n_kv_heads: int, head_dim: int, capacity_tokens: int = 1 << 16,
+                 dtype=torch.bfloat16, device=None):
+        self.n_kv_heads = int(n_kv_heads)
+        self.head_dim = int(head_dim)
+        self.dtype = dtype
+        self.device = device if device is not None else _device()
+        self._cap = max(int(capacity_tokens), 1)
+        self.k = torch.zeros((self._cap, n_kv_heads, head_dim), dtype=dtype, device=self.device)
+        self.v = torch.zeros_like(self.k)
+        self.pos = torch.full((self._cap,), _lib.POS_PAD_K, dtype=torch.int32, device=self.device)
+        self.seq = torch.full((self._cap,), _lib.SEQ_PAD_K, dtype=torch.int32, device=self.device)
+        self._used = 0
+        self._segs: dict[int, _Segment] = {}
+
+    # ---------------------------------------------------------------- storage
+    def _grow_arena(self, need_rows: int):
+        new_cap = self._cap
+        while new_cap < need_rows:
+            new_cap *= 2
+        if new_cap == self._cap:
+            return
+        for name, fill in (("k", 0), ("v", 0)):
+            old = getattr(self, name)
+            t = torch.zeros((new_cap,) + tuple(old.shape[1:]), dtype=old.dtype, device=self.device)
+            t[: self._used].copy_(old[: self._used])
+            setattr(self, name, t)
+        for name, fill in (("pos", _lib.POS_PAD_K), ("seq", _lib.SEQ_PAD_K)):
+            old = getattr(self, name)
+            t = torch.full((new_cap,), fill, dtype=torch.int32, device=self.device)
+            t[: self._used].copy_(old[: self._used])
+            setattr(self, name, t)
+        self._cap = new_cap
+
+    def _reserve(self, seq_id: int, extra: int) -> _Segment:
+        seg = self._segs.get(seq_id)
+        if seg is None:
+            seg = _Segment(start=self._used, cap=0, length=0, max_pos=-1)
+            self._segs[seq_id] = seg
+        if seg.length + extra <= seg.cap:
+            return seg
+        new_cap = max(2 * seg.cap, seg.length + extra, 64)
+        if seg.start + seg.cap == self._used:  # last segment: grow in place
+            self._grow_arena(seg.start + new_cap)
+            self._used = seg.start + new_cap
+            seg.cap = new_cap
+            return seg
+        start = self._used
+        self._grow_arena(start + new_cap)
+        if seg.length:
+            for t in (self.k, self.v, self.pos, self.seq):
+                t[start:start + seg.length].copy_(t[seg.start:seg.start + seg.length])
+        seg.start, seg.cap = start, new_cap
+        self._used = start + new_cap
+        return seg
+
+    # ---------------------------------------------------------------- SPEC API
+    def cached_len(self, seq_id: int) -> int:
+        seg = self._segs.get(seq_id)
+        return 0 if seg is None else seg.length
+
+    def seq_ids(self):
+        return list(self._segs.keys())
+
+    def segment(self, seq_id: int) -> tuple[int, int]:
+        """(first arena row, length) of a sequence's contiguous history."""
+        seg = self._segs.get(seq_id)
+        return (0, 0) if seg is None else (seg.start, seg.length)
+
+    def append(self, seq_id: int, k_block: EmbeddingBlock, v_block: EmbeddingBlock) -> int:
+        """Store the VALID rows of k/v; keeps position order."""
+        if tuple(k_block.data.shape) != tuple(v_block.data.shape):
+            raise ValueError("k/v shape mismatch")
+        if k_block.n_heads != self.n_kv_heads or k_block.head_dim != self.head_dim:
+            raise ValueError(f"kv blocks are [{k_block.n_heads} x {k_block.head_dim}] but cache "
+                             f"wants [{self.n_kv_heads} x {self.head_dim}]")
+        keep = k_block.valid & (k_block.seq_ids == seq_id)
+        idx = torch.nonzero(keep).flatten()
+        pos = k_block.positions[idx]
+        n = int(idx.numel())
+        if n == 0:
+            return self.cached_len(seq_id)
+        pos_host = pos.cpu().numpy()
+        return self._append_rows(seq_id, k_block.data[idx], v_block.data[idx], pos_host)
+
+    def append_rows(self, seq_id: int, k_rows: torch.Tensor, v_rows: torch.Tensor,
+                    positions: np.ndarray) -> int:
+        """Fast path with host-known positions (no device sync): rows are valid,
+        belong to seq_id and are in the given position order."""
+        return self._append_rows(seq_id, k_rows, v_rows, np.asarray(positions, np.int64))
+
+    def _append_rows(self, seq_id, k_rows, v_rows, pos_host: np.ndarray) -> int:
+        n = int(pos_host.shape[0])
+        if n == 0:
+            return self.cached_len(seq_id)
+        if np.any(np.diff(pos_host) <= 0):
+            order = np.argsort(pos_host, kind="stable")
+            sel = torch.from_numpy(order).to(self.device)
+            k_rows, v_rows, pos_host = k_rows[sel], v_rows[sel], pos_host[order]
+        seg = self._reserve(seq_id, n)
+        a = seg.start + seg.length
+        self.k[a:a + n].copy_(k_rows.to(self.dtype))
+        self.v[a:a + n].copy_(v_rows.to(self.dtype))
+        self.pos[a:a + n].copy_(torch.from_numpy(pos_host.astype(np.int32)))
+        self.seq[a:a + n].fill_(int(seq_id))
+        seg.length += n
+        if pos_host[0] <= seg.max_pos:
+            self._resort(seg)
+        seg.max_pos = max(seg.max_pos, int(pos_host[-1]))
+        return seg.length
+
+    def _resort(self, seg: _Segment):
+        a, b = seg.start, seg.start + seg.length
+        order = torch.argsort(self.pos[a:b], stable=True)
+        for t in (self.k, self.v, self.pos):
+            t[a:b].copy_(t[a:b][order])
+
+    def snapshot_padded(self, seq_id: int, max_len: int):
+        """(k, v) blocks of the cached rows padded with invalid rows to max_len
+        (SPEC.md:190-198); the cache itself is not modified."""
+        start, length = self.segment(seq_id)
+        if max_len < length:
+            raise ValueError(f"max_len {max_len} below cached_len {length}")
+        dev = self.device
+        kd = torch.zeros((max_len, self.n_kv_heads, self.head_dim), dtype=self.dtype, device=dev)
+        vd = torch.zeros_like(kd)
+        kd[:length].copy_(self.k[start:start + length])
+        vd[:length].copy_(self.v[start:start + length])
+        pos = torch.full((max_len,), -1, dtype=torch.int64, device=dev)
+        pos[:length].copy_(self.pos[start:start + length].to(torch.int64))
+        valid = torch.zeros(max_len, dtype=torch.bool, device=dev)
+        valid[:length] = True
+        seq = torch.full((max_len,), -1, dtype=torch.int64, device=dev)
+        seq[:length] = int(seq_id)
+        pos32 = torch.full((max_len,), _lib.POS_PAD_K, dtype=torch.int32, device=dev)
+        seq32 = torch.full((max_len,), _lib.SEQ_PAD_K, dtype=torch.int32, device=dev)
+        pos32[:length].copy_(self.pos[start:start + length])
+        seq32[:length] = int(seq_id)
+        kb = EmbeddingBlock(kd, pos, valid, seq, validate=False, n_valid=length)
+        vb = EmbeddingBlock(vd, pos, valid, seq, validate=False, n_valid=length)
+        kb._meta["k"] = (pos32, seq32)
+        vb._meta["k"] = (pos32, seq32)
+        return kb, vb

@@ -1,0 +1,571 @@
+"""Ring context-parallel protocols of arXiv 2411.01783 on B200 — the SPEC's ``ring_engine``.
+
+Reference: SPEC.md:221-303 (not shipped in pkg/) and PAPER.md Alg. 2-4
+(:283-303, :334-351, :353-370).  Two execution forms share one per-step
+compute path:
+
+* SPMD (one process per GPU): ``RingAttention(comm)`` with methods
+  ``pass_kv_prefill``, ``pass_q_prefill`` and ``pass_q_decode``.  Messages are
+  single flat device buffers (K | V | key metadata, or Q | query metadata) moved
+  with grouped NCCL send/recv issued before the step's attention kernel, so the
+  transfer of step j+1's block overlaps step j's compute; the compute stream
+  waits on the transfer only before it needs the block.
+* Simulated ranks (one process, one GPU, per-rank lists): ``ring_pass_kv_prefill``,
+  ``ring_pass_q_prefill``, ``ring_pass_q_decode`` with the SPEC's signatures —
+  the same kernels, messages read directly from the other ranks' buffers.
+
+Merge order.  pass-KV folds partials in arrival order (source ranks k, k-1, ...,
+k-N+1) inside the attention epilogue (rcp_attn_fwd mode MERGE — a running
+merge, so no N partials are ever stored).  pass-Q and decode merge the
+All2All-returned partials in that same order with the same fp32 merge code,
+so pass-KV and pass-Q are bit-identical.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .attention import (EmbeddingBlock, GqaConfig, PartialAttention, _bf16, attend_into,
+                        merge_rows_into)
+from .kv_cache import RankKvCache
+from .sharding import DecodePlan, ShardPlan, materialize_rank_block
+
+__all__ = [
+    "KvLayout",
+    "QLayout",
+    "RingAttention",
+    "RingTopology",
+    "StepTrace",
+    "TorchRingComm",
+    "ring_pass_kv_prefill",
+    "ring_pass_q_decode",
+    "ring_pass_q_prefill",
+]
+
+
+def _align(n: int, a: int = 256) -> int:
+    return (n + a - 1) // a * a
+
+
+@dataclass(frozen=True)
+class RingTopology:
+    """next(k) = (k+1) mod N, prev(k) = (k-1) mod N."""
+
+    n_ranks: int
+
+    def next(self, k: int) -> int:
+        return (k + 1) % self.n_ranks
+
+    def prev(self, k: int) -> int:
+        return (k - 1) % self.n_ranks
+
+    def source_at(self, k: int, step: int) -> int:
+        """Rank whose block is resident on rank k at ring step `step`."""
+        return (k - step) % self.n_ranks
+
+
+@dataclass
+class StepTrace:
+    """Per ring step: bytes sent per rank, message kind; per call: steps."""
+
+    records: list = field(default_factory=list)
+
+    def add(self, step: int, rank: int, kind: str, nbytes: int, pairs: int | None = None):
+        self.records.append((step, rank, kind, int(nbytes), pairs))
+
+    @property
+    def steps(self) -> int:
+        return len({(r[0], r[2]) for r in self.records})
+
+    def to_csv(self) -> str:
+        lines = ["step,rank,kind,bytes,pairs"]
+        for s, r, k, b, p in self.records:
+            lines.append(f"{s},{r},{k},{b},{'' if p is None else p}")
+        return "\n".join(lines) + "\n"
+
+
+# ------------------------------------------------------------------ message layouts
+@dataclass(frozen=True)
+class KvLayout:
+    """Flat KV message: K [L, Hkv, D] | V [L, Hkv, D] | pos int32 [L] | seq int32 [L]."""
+
+    tokens: int
+    n_kv_heads: int
+    head_dim: int
+    elem: int = 2
+
+    @property
+    def kv_bytes(self) -> int:
+        return self.tokens * self.n_kv_heads * self.head_dim * self.elem
+
+    @property
+    def v_off(self) -> int:
+        return _align(self.kv_bytes)
+
+    @property
+    def pos_off(self) -> int:
+        return self.v_off + _align(self.kv_bytes)
+
+    @property
+    def seq_off(self) -> int:
+        return self.pos_off + _align(4 * self.tokens)
+
+    @property
+    def nbytes(self) -> int:
+        return self.seq_off + _align(4 * self.tokens)
+
+    def views(self, buf: torch.Tensor, dtype=torch.bfloat16):
+        shape = (self.tokens, self.n_kv_heads, self.head_dim)
+        k = buf[: self.kv_bytes].view(dtype).view(shape)
+        v = buf[self.v_off:self.v_off + self.kv_bytes].view(dtype).view(shape)
+        pos = buf[self.pos_off:self.pos_off + 4 * self.tokens].view(torch.int32)
+        seq = buf[self.seq_off:self.seq_off + 4 * self.tokens].view(torch.int32)
+        return k, v, pos, seq
+
+
+@dataclass(frozen=True)
+class QLayout:
+    """Flat query message: Q [S, Hq, D] | pos int32 [S] | seq int32 [S]."""
+
+    tokens: int
+    n_q_heads: int
+    head_dim: int
+    elem: int = 2
+
+    @property
+    def q_bytes(self) -> int:
+        return self.tokens * self.n_q_heads * self.head_dim * self.elem
+
+    @property
+    def pos_off(self) -> int:
+        return _align(self.q_bytes)
+
+    @property
+    def seq_off(self) -> int:
+        return self.pos_off + _align(4 * self.tokens)
+
+    @property
+    def nbytes(self) -> int:
+        return self.seq_off + _align(4 * self.tokens)
+
+    def views(self, buf: torch.Tensor, dtype=torch.bfloat16):
+        q = buf[: self.q_bytes].view(dtype).view(self.tokens, self.n_q_heads, self.head_dim)
+        pos = buf[self.pos_off:self.pos_off + 4 * self.tokens].view(torch.int32)
+        seq = buf[self.seq_off:self.seq_off + 4 * self.tokens].view(torch.int32)
+        return q, pos, seq
+
+
+def kv_message_len(plan: ShardPlan) -> int:
+    """Equal-size KV message per rank: sum_i L^i (Alg. 2 line 2, sharding.py:95-103)."""
+    return plan.message_token_slots()
+
+
+def build_kv_message(plan: ShardPlan, cache: RankKvCache, buf: torch.Tensor | None = None):
+    """Per sequence i: [cached rows (position-sorted) | padding] up to L^i (Alg. 2)."""
+    lay = KvLayout(kv_message_len(plan), cache.n_kv_heads, cache.head_dim)
+    if buf is None:
+        buf = torch.empty(lay.nbytes, dtype=torch.uint8, device=cache.device)
+    k, v, pos, seq = lay.views(buf, cache.dtype)
+    off = 0
+    for i, sh in enumerate(plan.sequences):
+        L = plan.padded_len(i)
+        start, n = cache.segment(sh.spec.seq_id)
+        if n > L:
+            raise ValueError(f"sequence {sh.spec.seq_id}: cache holds {n} rows > L^i = {L}")
+        if n:
+            k[off:off + n].copy_(cache.k[start:start + n])
+            v[off:off + n].copy_(cache.v[start:start + n])
+            pos[off:off + n].copy_(cache.pos[start:start + n])
+            seq[off:off + n].copy_(cache.seq[start:start + n])
+        if L > n:
+            k[off + n:off + L].zero_()
+            v[off + n:off + L].zero_()
+            pos[off + n:off + L].fill_(_lib.POS_PAD_K)
+            seq[off + n:off + L].fill_(_lib.SEQ_PAD_K)
+        off += L
+    return lay, buf
+
+
+def append_new_tokens(plan: ShardPlan, rank: int, cache: RankKvCache, k_block: EmbeddingBlock,
+                      v_block: EmbeddingBlock) -> None:
+    """Append this rank's valid new K/V to its cache BEFORE the ring.
+    Positions are host-known from the plan, so no device sync is needed."""
+    off = 0
+    for i, sh in enumerate(plan.sequences):
+        loc = plan.rank_local_indices(i, rank)
+        slots = np.nonzero(loc >= 0)[0]
+        if slots.size:
+            rows = torch.from_numpy(slots + off).to(k_block.data.device)
+            if slots[-1] - slots[0] + 1 == slots.size:  # contiguous: plain slice
+                a, b = off + int(slots[0]), off + int(slots[-1]) + 1
+                kr, vr = k_block.data[a:b], v_block.data[a:b]
+            else:
+                kr, vr = k_block.data[rows], v_block.data[rows]
+            cache.append_rows(sh.spec.seq_id, kr, vr, sh.spec.cached_len + loc[slots])
+        off += loc.size
+
+
+# ------------------------------------------------------------------ transport
+class TorchRingComm:
+    """Ring transport over torch.distributed (NCCL between GPUs; gloo works for
+    CPU tests).  P2P ops are issued on the current stream's order: NCCL's stream
+    waits for work already queued, so a transfer issued before a step's kernel
+    overlaps it; ``wait`` makes the current stream wait for the transfer."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.topo = RingTopology(self.world)
+
+    def _g(self, r: int) -> int:
+        return r if self.group is None else self.dist.get_global_rank(self.group, r)
+
+    def exchange(self, send: torch.Tensor, recv: torch.Tensor):
+        d = self.dist
+        ops = [d.P2POp(d.isend, send, self._g(self.topo.next(self.rank)), self.group),
+               d.P2POp(d.irecv, recv, self._g(self.topo.prev(self.rank)), self.group)]
+        return d.batch_isend_irecv(ops)
+
+    def all_to_all(self, sends: list, recvs: list):
+        """sends[r] -> rank r, recvs[r] <- rank r; own entry copied locally
+        (N-1 pairwise exchanges in one fixed schedule)."""
+        d = self.dist
+        ops = []
+        for r in range(self.world):
+            if r == self.rank:
+                continue
+            ops.append(d.P2POp(d.isend, sends[r], self._g(r), self.group))
+            ops.append(d.P2POp(d.irecv, recvs[r], self._g(r), self.group))
+        works = d.batch_isend_irecv(ops) if ops else []
+        recvs[self.rank].copy_(sends[self.rank])
+        return works
+
+    @staticmethod
+    def wait(works):
+        for w in works or []:
+            w.wait()
+
+
+# ------------------------------------------------------------------ compute hooks
+def _cuda_attend(q, q_pos, q_seq, k, v, k_pos, k_seq, cfg: GqaConfig, out, lse, mode, ws=None):
+    attend_into(q, (q_pos, q_seq), k, v, (k_pos, k_seq), cfg.n_query_heads, cfg.n_kv_heads,
+                cfg.scale, out, lse, mode, ws)
+
+
+def _cuda_merge(o_parts, l_parts, out, lse):
+    merge_rows_into(o_parts, l_parts, out, lse)
+
+
+class RingAttention:
+    """SPMD ring attention for one rank.  ``attend``/``merge`` default to the
+    sm_100a kernels; tests inject oracle callables to check the schedule on CPU."""
+
+    def __init__(self, comm, attend=None, merge=None, device=None):
+        self.comm = comm
+        self.attend = attend or _cuda_attend
+        self.merge = merge or _cuda_merge
+        self.device = device
+        self._bufs = {}
+        self.trace: StepTrace | None = None
+
+    def _buf(self, key, nbytes, device):
+        b = self._bufs.get(key)
+        if b is None or b.numel() < nbytes or b.device != device:
+            b = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            self._bufs[key] = b
+        return b[:nbytes]
+
+    # -------------------------------------------------------------- Alg. 2
+    def pass_kv(self, q, q_pos, q_seq, kv_lay: KvLayout, kv_msg: torch.Tensor, cfg: GqaConfig,
+                out: torch.Tensor, lse: torch.Tensor, dtype=torch.bfloat16):
+        """Ring pass-KV over prepared buffers: q [S, Hq, D], kv_msg the local
+        flat KV message.  Writes the merged (out, lse) for this rank's queries."""
+        n, k = self.comm.world, self.comm.rank
+        dev = kv_msg.device
+        bufs = [self._buf(("kv", 0), kv_lay.nbytes, dev), self._buf(("kv", 1), kv_lay.nbytes, dev)]
+        cur = kv_msg
+        for step in range(n):
+            works = None
+            nxt = None
+            if step < n - 1:
+                nxt = bufs[step % 2]
+                works = self.comm.exchange(cur, nxt)
+                if self.trace is not None:
+                    self.trace.add(step, k, "KV", kv_lay.nbytes)
+            kk, vv, kp, ks = kv_lay.views(cur, dtype)
+            self.attend(q, q_pos, q_seq, kk, vv, kp, ks, cfg, out, lse,
+                        _lib.MODE_OVERWRITE if step == 0 else _lib.MODE_MERGE)
+            self.comm.wait(works)
+            cur = nxt
+        return out, lse
+
+    def pass_kv_prefill(self, plan: ShardPlan, cache: RankKvCache, q_block: EmbeddingBlock,
+                        k_block: EmbeddingBlock, v_block: EmbeddingBlock, cfg: GqaConfig) -> PartialAttention:
+        """Alg. 2 for this rank: append new K/V to the cache, build the padded
+        KV message, run the ring, return the merged partial of the rank's queries."""
+        k = self.comm.rank
+        append_new_tokens(plan, k, cache, k_block, v_block)
+        lay = KvLayout(kv_message_len(plan), cache.n_kv_heads, cache.head_dim)
+        msg = self._buf(("kv", "local"), lay.nbytes, cache.device)
+        build_kv_message(plan, cache, msg)
+        qd = _bf16(q_block.data)
+        qp, qs = q_block.meta32("q")
+        out = torch.empty((q_block.n_tokens, cfg.n_query_heads, cfg.head_dim), dtype=torch.float32,
+                          device=qd.device)
+        lse = torch.empty((q_block.n_tokens, cfg.n_query_heads), dtype=torch.float32, device=qd.device)
+        self.pass_kv(qd, qp, qs, lay, msg, cfg, out, lse, cache.dtype)
+        blk = EmbeddingBlock(out, q_block.positions, q_block.valid, q_block.seq_ids, validate=False,
+                             n_valid=q_block.n_valid)
+        return PartialAttention(blk, lse)
+
+    # -------------------------------------------------------------- Alg. 3
+    def pass_q(self, q_lay: QLayout, q_msg: torch.Tensor, kk, vv, kp, ks, cfg: GqaConfig,
+               out: torch.Tensor, lse: torch.Tensor, dtype=torch.bfloat16):
+        """Ring pass-Q over prepared buffers, then All2All of the partials and the
+        merge in pass-KV arrival order."""
+        n, k = self.comm.world, self.comm.rank
+        dev = q_msg.device
+        S, H, D = q_lay.tokens, cfg.n_query_heads, cfg.head_dim
+        send_o = [torch.empty((S, H, D), dtype=torch.float32, device=dev) for _ in range(n)]
+        send_l = [torch.empty((S, H), dtype=torch.float32, device=dev) for _ in range(n)]
+        bufs = [self._buf(("q", 0), q_lay.nbytes, dev), self._buf(("q", 1), q_lay.nbytes, dev)]
+        cur = q_msg
+        for step in range(n):
+            src = (k - step) % n
+            works = None
+            nxt = None
+            if step < n - 1:
+                nxt = bufs[step % 2]
+                works = self.comm.exchange(cur, nxt)
+                if self.trace is not None:
+                    self.trace.add(step, k, "Q", q_lay.nbytes)
+            qq, qp, qs = q_lay.views(cur, dtype)
+            self.attend(qq, qp, qs, kk, vv, kp, ks, cfg, send_o[src], send_l[src], _lib.MODE_OVERWRITE)
+            self.comm.wait(works)
+            cur = nxt
+        recv_o = [torch.empty_like(send_o[0]) for _ in range(n)]
+        recv_l = [torch.empty_like(send_l[0]) for _ in range(n)]
+        w1 = self.comm.all_to_all(send_o, recv_o)
+        w2 = self.comm.all_to_all(send_l, recv_l)
+        if self.trace is not None:
+            self.trace.add(n - 1, k, "A2A", (n - 1) * (send_o[0].numel() + send_l[0].numel()) * 4)
+        self.comm.wait(w1)
+        self.comm.wait(w2)
+        order = [(k - j) % n for j in range(n)]
+        self.merge([recv_o[s] for s in order], [recv_l[s] for s in order], out, lse)
+        return out, lse
+
+    def pass_q_prefill(self, plan: ShardPlan, cache: RankKvCache, q_block: EmbeddingBlock,
+                       k_block: EmbeddingBlock, v_block: EmbeddingBlock, cfg: GqaConfig) -> PartialAttention:
+        """Alg. 3 for this rank: KV stays resident (cache + new tokens), Q rotates."""
+        k = self.comm.rank
+        append_new_tokens(plan, k, cache, k_block, v_block)
+        lay, msg = build_kv_message(plan, cache, self._buf(("kv", "local"),
+                                                           KvLayout(kv_message_len(plan), cache.n_kv_heads,
+                                                                    cache.head_dim).nbytes, cache.device))
+        kk, vv, kp, ks = lay.views(msg, cache.dtype)
+        qlay = QLayout(q_block.n_tokens, cfg.n_query_heads, cfg.head_dim)
+        qmsg = self._buf(("q", "local"), qlay.nbytes, cache.device)
+        qq, qp, qs = qlay.views(qmsg)
+        qq.copy_(_bf16(q_block.data))
+        p32, s32 = q_block.meta32("q")
+        qp.copy_(p32)
+        qs.copy_(s32)
+        out = torch.empty((q_block.n_tokens, cfg.n_query_heads, cfg.head_dim), dtype=torch.float32,
+                          device=cache.device)
+        lse = torch.empty((q_block.n_tokens, cfg.n_query_heads), dtype=torch.float32, device=cache.device)
+        self.pass_q(qlay, qmsg, kk, vv, kp, ks, cfg, out, lse)
+        blk = EmbeddingBlock(out, q_block.positions, q_block.valid, q_block.seq_ids, validate=False,
+                             n_valid=q_block.n_valid)
+        return PartialAttention(blk, lse)
+
+    # -------------------------------------------------------------- Alg. 4
+    def pass_q_decode(self, plan: DecodePlan, cache: RankKvCache, q_tok: torch.Tensor,
+                      k_tok: torch.Tensor, v_tok: torch.Tensor, positions, cfg: GqaConfig):
+        """Batched ring pass-Q decode for this rank.
+
+        q_tok/k_tok/v_tok: [slots_per_rank, H, D] — this rank's assigned decode
+        tokens in ``plan.assignments[rank]`` order (padded slots ignored);
+        positions: their global positions.  The owner appends its tokens' K/V
+        first (the query attends to itself), then queries rotate,
+        every rank attends the visitors against its cached shard of their
+        sequences, and an All2All returns the partials to the owner, merged in
+        pass-KV arrival order.  Returns (out [slots, Hq, D], lse [slots, Hq])."""
+        n, k = self.comm.world, self.comm.rank
+        mine = plan.assignments[k]
+        slots = plan.slots_per_rank
+        for j, (sid, _b) in enumerate(mine):
+            cache.append_rows(sid, k_tok[j:j + 1], v_tok[j:j + 1], [int(positions[j])])
+        dev = cache.device
+        H, D = cfg.n_query_heads, cfg.head_dim
+        qlay = QLayout(slots, H, D)
+        qmsg = self._buf(("dq", "local"), qlay.nbytes, dev)
+        qq, _, _ = qlay.views(qmsg)
+        qq.zero_()
+        if mine:
+            qq[: len(mine)].copy_(_bf16(q_tok[: len(mine)]))
+        # per step: kv segment of every visiting slot (host-known from the plan)
+        starts = np.zeros((n, slots), np.int64)
+        lens = np.zeros((n, slots), np.int64)
+        for step in range(n):
+            src = (k - step) % n
+            for j, (sid, _b) in enumerate(plan.assignments[src]):
+                starts[step, j], lens[step, j] = cache.segment(sid)
+        st_d = torch.from_numpy(starts).to(dev)
+        ln_d = torch.from_numpy(lens).to(dev)
+        max_len = int(lens.max()) if lens.size else 0
+        lib = _lib.load()
+        ws_bytes = lib.rcp_decode_workspace_bytes(slots, H, max(max_len, 1))
+        ws = self._buf(("dws",), max(ws_bytes, 32), dev)
+        send_o = [torch.empty((slots, H, D), dtype=torch.float32, device=dev) for _ in range(n)]
+        send_l = [torch.empty((slots, H), dtype=torch.float32, device=dev) for _ in range(n)]
+        bufs = [self._buf(("dq", 0), qlay.nbytes, dev), self._buf(("dq", 1), qlay.nbytes, dev)]
+        cur = qmsg
+        for step in range(n):
+            src = (k - step) % n
+            works = None
+            nxt = None
+            if step < n - 1:
+                nxt = bufs[step % 2]
+                works = self.comm.exchange(cur, nxt)
+                if self.trace is not None:
+                    self.trace.add(step, k, "Q", qlay.nbytes)
+            q_cur, _, _ = qlay.views(cur)
+            _lib.check(lib.rcp_decode_attn(
+                _lib.ptr(q_cur), _lib.ptr(cache.k), _lib.ptr(cache.v), cache.k.stride(0),
+                _lib.ptr(st_d[step]), _lib.ptr(ln_d[step]), slots, max(max_len, 1), H,
+                cfg.n_kv_heads, D, float(cfg.scale), _lib.ptr(send_o[src]), _lib.ptr(send_l[src]),
+                _lib.ptr(ws), ws.numel(), _lib.stream_handle()))
+            self.comm.wait(works)
+            cur = nxt
+        recv_o = [torch.empty_like(send_o[0]) for _ in range(n)]
+        recv_l = [torch.empty_like(send_l[0]) for _ in range(n)]
+        w1 = self.comm.all_to_all(send_o, recv_o)
+        w2 = self.comm.all_to_all(send_l, recv_l)
+        self.comm.wait(w1)
+        self.comm.wait(w2)
+        out = torch.empty((slots, H, D), dtype=torch.float32, device=dev)
+        lse = torch.empty((slots, H), dtype=torch.float32, device=dev)
+        order = [(k - j) % n for j in range(n)]
+        self.merge([recv_o[s] for s in order], [recv_l[s] for s in order], out, lse)
+        return out, lse
+
+
+# ------------------------------------------------------------------ simulated ranks (SPEC signatures)
+class _LocalComm:
+    """In-process stand-in used by the simulated-rank drivers: exchanges are
+    resolved by the driver, so this only carries rank/world."""
+
+    def __init__(self, rank, world):
+        self.rank, self.world = rank, world
+
+
+def ring_pass_kv_prefill(plan: ShardPlan, caches: list, q_blocks: list, k_blocks: list,
+                         v_blocks: list, cfg: GqaConfig, trace: StepTrace | None = None):
+    """Alg. 2 over N simulated ranks on one GPU.  Returns the
+    per-rank merged PartialAttention list (and fills `trace` if given)."""
+    n = plan.n_ranks
+    for r in range(n):
+        append_new_tokens(plan, r, caches[r], k_blocks[r], v_blocks[r])
+    msgs = [build_kv_message(plan, caches[r]) for r in range(n)]
+    outs = []
+    for r in range(n):
+        q = q_blocks[r]
+        qd = _bf16(q.data)
+        qp, qs = q.meta32("q")
+        out = torch.empty((q.n_tokens, cfg.n_query_heads, cfg.head_dim), dtype=torch.float32, device=qd.device)
+        lse = torch.empty((q.n_tokens, cfg.n_query_heads), dtype=torch.float32, device=qd.device)
+        for step in range(n):
+            src = (r - step) % n
+            lay, buf = msgs[src]
+            kk, vv, kp, ks = lay.views(buf, caches[src].dtype)
+            _cuda_attend(qd, qp, qs, kk, vv, kp, ks, cfg, out, lse,
+                         _lib.MODE_OVERWRITE if step == 0 else _lib.MODE_MERGE)
+            if trace is not None and step < n - 1:
+                trace.add(step, r, "KV", lay.nbytes)
+        outs.append(PartialAttention(EmbeddingBlock(out, q.positions, q.valid, q.seq_ids, validate=False,
+                                                    n_valid=q.n_valid), lse))
+    return outs
+
+
+def ring_pass_q_prefill(plan: ShardPlan, caches: list, q_blocks: list, k_blocks: list,
+                        v_blocks: list, cfg: GqaConfig, trace: StepTrace | None = None):
+    """Alg. 3 over N simulated ranks: rank s computes O_r^s for
+    every visiting Q_r against its resident KV; the All2All returns them and rank
+    r merges in pass-KV arrival order — bit-identical to ring_pass_kv_prefill."""
+    n = plan.n_ranks
+    for r in range(n):
+        append_new_tokens(plan, r, caches[r], k_blocks[r], v_blocks[r])
+    msgs = [build_kv_message(plan, caches[r]) for r in range(n)]
+    held = {}
+    for s in range(n):  # resident KV rank
+        lay, buf = msgs[s]
+        kk, vv, kp, ks = lay.views(buf, caches[s].dtype)
+        for step in range(n):
+            r = (s - step) % n  # visiting query rank
+            q = q_blocks[r]
+            o = torch.empty((q.n_tokens, cfg.n_query_heads, cfg.head_dim), dtype=torch.float32, device=kk.device)
+            l = torch.empty((q.n_tokens, cfg.n_query_heads), dtype=torch.float32, device=kk.device)
+            qp, qs = q.meta32("q")
+            _cuda_attend(_bf16(q.data), qp, qs, kk, vv, kp, ks, cfg, o, l, _lib.MODE_OVERWRITE)
+            held[(r, s)] = (o, l)
+            if trace is not None and step < n - 1:
+                trace.add(step, s, "Q", QLayout(q.n_tokens, cfg.n_query_heads, cfg.head_dim).nbytes)
+    outs = []
+    for r in range(n):
+        order = [(r - j) % n for j in range(n)]
+        q = q_blocks[r]
+        out = torch.empty_like(held[(r, r)][0])
+        lse = torch.empty_like(held[(r, r)][1])
+        _cuda_merge([held[(r, s)][0] for s in order], [held[(r, s)][1] for s in order], out, lse)
+        if trace is not None:
+            trace.add(n - 1, r, "A2A", (n - 1) * (out.numel() + lse.numel()) * 4)
+        outs.append(PartialAttention(EmbeddingBlock(out, q.positions, q.valid, q.seq_ids, validate=False,
+                                                    n_valid=q.n_valid), lse))
+    return outs
+
+
+def ring_pass_q_decode(plan: DecodePlan, caches: list, q_tok: torch.Tensor, k_tok: torch.Tensor,
+                       v_tok: torch.Tensor, positions, cfg: GqaConfig):
+    """Alg. 4 over N simulated ranks.  q_tok/k_tok/v_tok are
+    [B, H, D] in batch order; positions[b] the token's global position.
+    Returns (out [B, Hq, D], lse [B, Hq]) in batch order."""
+    n = plan.n_ranks
+    B = len(plan.batch)
+    for b, sid in enumerate(plan.batch):
+        caches[plan.owner(b)].append_rows(sid, k_tok[b:b + 1], v_tok[b:b + 1], [int(positions[b])])
+    H, D = cfg.n_query_heads, cfg.head_dim
+    dev = caches[0].device
+    lib = _lib.load()
+    qb = _bf16(q_tok).contiguous()
+    out = torch.empty((B, H, D), dtype=torch.float32, device=dev)
+    lse = torch.empty((B, H), dtype=torch.float32, device=dev)
+    for b, sid in enumerate(plan.batch):
+        owner = plan.owner(b)
+        order = [(owner - j) % n for j in range(n)]
+        parts_o, parts_l = [], []
+        for s in order:
+            start, length = caches[s].segment(sid)
+            st = torch.tensor([start], dtype=torch.int64, device=dev)
+            ln = torch.tensor([length], dtype=torch.int64, device=dev)
+            o = torch.empty((1, H, D), dtype=torch.float32, device=dev)
+            l = torch.empty((1, H), dtype=torch.float32, device=dev)
+            ws_bytes = lib.rcp_decode_workspace_bytes(1, H, max(length, 1))
+            ws = torch.empty(max(ws_bytes, 32), dtype=torch.uint8, device=dev)
+            _lib.check(lib.rcp_decode_attn(
+                _lib.ptr(qb[b:b + 1]), _lib.ptr(caches[s].k), _lib.ptr(caches[s].v), caches[s].k.stride(0),
+                _lib.ptr(st), _lib.ptr(ln), 1, max(length, 1), H, cfg.n_kv_heads, D, float(cfg.scale),
+                _lib.ptr(o), _lib.ptr(l), _lib.ptr(ws), ws.numel(), _lib.stream_handle()))
+            parts_o.append(o)
+            parts_l.append(l)
+        _cuda_merge(parts_o, parts_l, out[b:b + 1], lse[b:b + 1])
+    return out, lse
