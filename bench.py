@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""Benchmark of the CP ring-attention prefill path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 8b|405b|405b-1m]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1, one rank per GPU)
+    python bench.py --impl reference ...                   (CPU reference arm)
+
+One step = one full context-parallel attention call of one layer for a fused
+batch of one sequence: load-balanced sharding of Q/K/V on every rank
+(rcp_shard_gather), KV-cache append + padded KV message, N ring steps of
+tcgen05 attention with the running LSE merge, NCCL send/recv overlapped.
+Default workload = BASELINE configs[1]: Llama-3-8B-shaped layer (32 Q / 8 KV
+heads, d=128), 131072-token full prefill, pass-KV, bf16, CP = N GPUs (total
+work fixed: strong scaling).  Inputs (1 GB Q, 268 MB K/V at CP1) exceed the
+126 MB L2, so no flush is needed between steps.
+
+Prints ONE JSON line on rank 0 (metric, value = whole-job TFLOP/s, roofline of
+the attention kernel, CPU baseline of the oracle port, e2e through the public
+API with host buffers, clocks sampled during the timed region).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CP prefill attn latency (ms) + TFLOPS/GPU at 128K/1M tokens, CP=1/2/4/8"
+CONFIGS = {
+    "8b": dict(workload="llama3-8b-attn-128k-full-prefill-pass-kv", hq=32, hkv=8, T=131072),
+    "405b": dict(workload="llama3-405b-attn-128k-full-prefill-pass-kv", hq=128, hkv=8, T=131072),
+    "405b-1m": dict(workload="llama3-405b-attn-1m-full-prefill-pass-kv", hq=128, hkv=8, T=1048576),
+}
+D = 128
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return dict(hbm=float(p["hbm_gbs"]), bf16=float(p["bf16_tflops"]),
+                    bf16_sus=float(p.get("bf16_tflops_sustained", p["bf16_tflops"])), src="measured")
+    except Exception:
+        return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+
+
+def causal_pairs(q_pos: np.ndarray, k_pos: np.ndarray) -> int:
+    """Admitted pairs of one sequence: #keys with position <= query position."""
+    ks = np.sort(k_pos)
+    return int(np.searchsorted(ks, q_pos, side="right").sum())
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.idx)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(self.NAMES, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------- CPU arms
+def _oracle_sample(T, hq, hkv, rows, seed=7):
+    """Bounded sample of the same workload for the oracle port: `rows` query
+    rows spread over the sequence, attending to every key (causal)."""
+    from oracle import ringcp_oracle as orc
+
+    rng = np.random.default_rng(seed)
+    q_pos = np.linspace(T // 2, T - 1, rows).astype(np.int64)
+    q = orc.blk_from_tokens(rng.standard_normal((rows, hq, D)).astype(np.float32), q_pos)
+    k = orc.blk_from_tokens(rng.standard_normal((T, hkv, D)).astype(np.float32), np.arange(T))
+    v = orc.blk_from_tokens(rng.standard_normal((T, hkv, D)).astype(np.float32), np.arange(T))
+    pairs = int((q_pos + 1).sum())
+    return q, k, v, pairs
+
+
+def _oracle_worker(args):
+    T, hq, hkv, rows, seed = args
+    from oracle import ringcp_oracle as orc
+
+    q, k, v, pairs = _oracle_sample(T, hq, hkv, rows, seed)
+    t0 = time.perf_counter()
+    orc.gqa(q, k, v, hkv)
+    return time.perf_counter() - t0, pairs
+
+
+def cpu_baseline_port(T, hq, hkv, rows=16):
+    """Oracle port (the reference's numpy algorithm), single process = 1 core."""
+    dt, pairs = _oracle_worker((T, hq, hkv, rows, 7))
+    flops = 4.0 * D * hq * pairs
+    return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": 1, "kind": "port",
+            "sample": f"{rows} query rows x {T} keys x {hq}/{hkv} heads (positions {T // 2}..{T - 1}), "
+                      f"oracle gqa {dt:.2f} s"}
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the reference algorithm (oracle port; the reference is
+    pure Python/numpy) on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    T, hq, hkv = cfg["T"], cfg["hq"], cfg["hkv"]
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    rows_per = 2
+    jobs = [(T, hq, hkv, rows_per, 100 + i) for i in range(cores)]
+    ctx = mp.get_context("fork")
+    vals = []
+    with ctx.Pool(cores) as pool:
+        for it in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            res = pool.map(_oracle_worker, jobs)
+            dt = time.perf_counter() - t0
+            pairs = sum(r[1] for r in res)
+            if it >= args.warmup:
+                vals.append(4.0 * D * hq * pairs / dt / 1e12)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "seq_len": T, "n_q_heads": hq, "n_kv_heads": hkv,
+                   "head_dim": D, "cp": world},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                         "sample": f"{cores} processes x {rows_per} query rows x {T} keys per step"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------- GPU arm
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_01783_b200 as rc
+    from paper_2411_01783_b200 import _lib
+    from paper_2411_01783_b200.kv_cache import RankKvCache
+    from paper_2411_01783_b200.ring import RingAttention, TorchRingComm, _LocalComm, _cuda_attend
+    from paper_2411_01783_b200.sharding import SequenceSpec, materialize_rank_block, plan_full_prefill
+
+    _lib.load()
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    T, hq, hkv = cfg["T"], cfg["hq"], cfg["hkv"]
+    gcfg = rc.GqaConfig(hq, hkv, D)
+    plan = plan_full_prefill([SequenceSpec(0, 0, T)], world)
+
+    # synthetic bf16 inputs, identical on every rank / every CP size (fixed seeds)
+    gen = torch.Generator(device=dev)
+    tens = {}
+    for name, h, seed in (("q", hq, 11), ("k", hkv, 12), ("v", hkv, 13)):
+        gen.manual_seed(seed)
+        tens[name] = torch.randn((T, h, D), generator=gen, device=dev, dtype=torch.bfloat16)
+
+    comm = TorchRingComm() if world > 1 else _LocalComm(0, 1)
+    ring = RingAttention(comm)
+    cache = RankKvCache(hkv, D, capacity_tokens=plan.total_query_slots() + 4096, device=dev)
+
+    # exact algorithmic work: admitted pairs of this rank's queries vs every source block
+    qpos = np.concatenate([plan.rank_local_indices(0, rank)])
+    qpos = qpos[qpos >= 0]
+    rank_pairs = causal_pairs(qpos, np.arange(T))
+    total_pairs = T * (T + 1) // 2
+    flops_rank = 4.0 * D * hq * rank_pairs
+    flops_total = 4.0 * D * hq * total_pairs
+
+    # per-launch CUDA events around the attention kernel (launching stream)
+    events = []
+    timing = {"on": False}
+
+    def timed_attend(*a, **kw):
+        if timing["on"]:
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record()
+            _cuda_attend(*a, **kw)
+            e.record()
+            events.append((s, e))
+        else:
+            _cuda_attend(*a, **kw)
+
+    ring.attend = timed_attend
+
+    def step():
+        cache.reset()
+        qb = materialize_rank_block(plan, rank, [tens["q"]])
+        kb = materialize_rank_block(plan, rank, [tens["k"]])
+        vb = materialize_rank_block(plan, rank, [tens["v"]])
+        return ring.pass_kv_prefill(plan, cache, qb, kb, vb, gcfg)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    n0 = _lib.launch_count
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    timing["on"] = True
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        t0.record()
+        for _ in range(args.steps):
+            step()
+        t1.record()
+        barrier()
+    timing["on"] = False
+    launches = _lib.launch_count - n0
+    ms_rank = t0.elapsed_time(t1) / args.steps
+    ms = max_over_ranks(ms_rank)
+    attn_ms = [s.elapsed_time(e) for s, e in events]
+    attn_avg_ms = sum(attn_ms) / len(attn_ms)
+    per_launch_flops = flops_rank / world  # world ring steps per call
+    achieved = per_launch_flops / (attn_avg_ms * 1e-3) / 1e12
+    attn_share = sum(attn_ms) / (ms_rank * args.steps)
+
+    # ---------------- e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        host = {n: t.cpu().pin_memory() for n, t in tens.items()}
+        s_slots = plan.total_query_slots()
+        out_host = torch.empty((s_slots, hq, D), dtype=torch.float32).pin_memory()
+        lse_host = torch.empty((s_slots, hq), dtype=torch.float32).pin_memory()
+        h2d = 0
+        for n, t in host.items():
+            h2d += t[0].numel() * t.element_size() * (T // world)  # rank's two chunks
+        d2h = out_host.numel() * 4 + lse_host.numel() * 4
+
+        def e2e_step():
+            cache.reset()
+            qb = materialize_rank_block(plan, rank, [host["q"]])
+            kb = materialize_rank_block(plan, rank, [host["k"]])
+            vb = materialize_rank_block(plan, rank, [host["v"]])
+            part = ring.pass_kv_prefill(plan, cache, qb, kb, vb, gcfg)
+            out_host.copy_(part.output.data, non_blocking=True)
+            lse_host.copy_(part.lse, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record()
+        barrier()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+        e2e = {"value": flops_total / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+    if rank != 0:
+        return
+    pk = peaks()
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tj = json.load(f)
+            traffic = tj.get(args.config, {}).get(str(world))
+        except Exception:
+            traffic = None
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_port(T, hq, hkv, rows=args.cpu_rows)
+    value = flops_total / (ms * 1e-3) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic",
+        "config": {"workload": cfg["workload"], "seq_len": T, "n_q_heads": hq, "n_kv_heads": hkv,
+                   "head_dim": D, "cp": world, "protocol": "pass_kv", "parallelism": f"cp{world}",
+                   "l2": "inputs larger than L2 (Q %.0f MB, K/V %.0f MB per rank)" % (
+                       T // world * hq * D * 2 / 1e6, T // world * hkv * D * 2 / 1e6)},
+        "latency_ms": ms, "tflops_per_gpu": value / world,
+        "roofline": {"bound": "tensor", "kernel": "attn_fwd_kernel", "achieved": achieved,
+                     "peak": pk["bf16_sus"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_sus"],
+                     "peak_kind": f"{pk['src']} sustained bf16 (kernel runs inside a long step)",
+                     "frac_of_burst": achieved / pk["bf16"], "traffic": traffic,
+                     "launch_ms": attn_avg_ms, "flops_per_launch": per_launch_flops,
+                     "attn_share_of_step": attn_share},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="8b", choices=sorted(CONFIGS))
+    ap.add_argument("--seq-len", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=16)
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.seq_len:
+        cfg["T"] = args.seq_len
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -57,6 +57,16 @@ SIGNATURES = {
 
 _lib = None
 
+# Kernel launches issued through this binding (per C-ABI call: rcp_attn_fwd 3 =
+# two tile summaries + attention; rcp_decode_attn 2; every other call 1).
+LAUNCHES_PER_CALL = {"rcp_attn_fwd": 3, "rcp_decode_attn": 2}
+launch_count = 0
+
+
+def count(name: str) -> None:
+    global launch_count
+    launch_count += LAUNCHES_PER_CALL.get(name, 1)
+
 
 def load() -> ctypes.CDLL:
     """Load (once) and type the C-ABI library; raise if it is absent."""

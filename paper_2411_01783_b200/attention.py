@@ -232,6 +232,7 @@ class EmbeddingBlock:
             pos = torch.empty(n, dtype=torch.int32, device=dev)
             seq = torch.empty(n, dtype=torch.int32, device=dev)
             lib = _lib.load()
+            _lib.count("rcp_fold_meta")
             _lib.check(lib.rcp_fold_meta(_lib.ptr(self._positions), _lib.ptr(self._seq_ids),
                                          _lib.ptr(self._valid), n, 1 if role == "k" else 0,
                                          _lib.ptr(pos), _lib.ptr(seq), _lib.stream_handle()))
@@ -307,6 +308,7 @@ def attend_into(q_data: torch.Tensor, q_meta, k_data: torch.Tensor, v_data: torc
     need = lib.rcp_attn_workspace_bytes(tq, tk)
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(max(need, 32), dtype=torch.uint8, device=q_data.device)
+    _lib.count("rcp_attn_fwd")
     _lib.check(lib.rcp_attn_fwd(
         _lib.ptr(q_data), q_data.stride(0), _lib.ptr(k_data), k_data.stride(0),
         _lib.ptr(v_data), v_data.stride(0),
@@ -353,6 +355,7 @@ def merge_rows_into(o_parts, lse_parts, out: torch.Tensor, lse_out: torch.Tensor
     lib = _lib.load()
     n = len(o_parts)
     rows = lse_out.numel()
+    _lib.count("rcp_merge_attn")
     _lib.check(lib.rcp_merge_attn(_lib.ptr_array([_lib.ptr(t) for t in o_parts]),
                                   _lib.ptr_array([_lib.ptr(t) for t in lse_parts]), n, rows,
                                   out.shape[-1], _lib.ptr(out), _lib.ptr(lse_out),

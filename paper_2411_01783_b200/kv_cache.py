@@ -94,6 +94,11 @@ class RankKvCache:
         self._used = start + new_cap
         return seg
 
+    def reset(self) -> None:
+        """Forget every sequence (keeps the arena allocation)."""
+        self._used = 0
+        self._segs.clear()
+
     # ---------------------------------------------------------------- SPEC API
     def cached_len(self, seq_id: int) -> int:
         seg = self._segs.get(seq_id)

@@ -440,6 +440,7 @@ class RingAttention:
                 if self.trace is not None:
                     self.trace.add(step, k, "Q", qlay.nbytes)
             q_cur, _, _ = qlay.views(cur)
+            _lib.count("rcp_decode_attn")
             _lib.check(lib.rcp_decode_attn(
                 _lib.ptr(q_cur), _lib.ptr(cache.k), _lib.ptr(cache.v), cache.k.stride(0),
                 _lib.ptr(st_d[step]), _lib.ptr(ln_d[step]), slots, max(max_len, 1), H,
@@ -467,6 +468,10 @@ class _LocalComm:
 
     def __init__(self, rank, world):
         self.rank, self.world = rank, world
+
+    @staticmethod
+    def wait(works):
+        assert not works
 
 
 def ring_pass_kv_prefill(plan: ShardPlan, caches: list, q_blocks: list, k_blocks: list,
@@ -561,6 +566,7 @@ def ring_pass_q_decode(plan: DecodePlan, caches: list, q_tok: torch.Tensor, k_to
             l = torch.empty((1, H), dtype=torch.float32, device=dev)
             ws_bytes = lib.rcp_decode_workspace_bytes(1, H, max(length, 1))
             ws = torch.empty(max(ws_bytes, 32), dtype=torch.uint8, device=dev)
+            _lib.count("rcp_decode_attn")
             _lib.check(lib.rcp_decode_attn(
                 _lib.ptr(qb[b:b + 1]), _lib.ptr(caches[s].k), _lib.ptr(caches[s].v), caches[s].k.stride(0),
                 _lib.ptr(st), _lib.ptr(ln), 1, max(length, 1), H, cfg.n_kv_heads, D, float(cfg.scale),

@@ -1,0 +1,184 @@
+"""GPU: device sharding bit-exact vs the reference, ring pass-KV / pass-Q /
+decode over simulated ranks vs the reference-composed oracle."""
+
+import numpy as np
+import pytest
+
+from oracle import ringcp_oracle as orc
+from tests import _golden as G
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rc():
+    import paper_2411_01783_b200 as rc
+
+    return rc
+
+
+def test_materialize_bit_exact_vs_reference(rc):
+    import torch
+
+    from paper_2411_01783_b200.sharding import (SequenceSpec, materialize_rank_block,
+                                                plan_full_prefill, plan_partial_prefill)
+
+    cases = G.js("shard.json")
+    z = G.npz("shard.npz")
+    for ci, c in enumerate(cases):
+        if f"s{ci}__in0" not in z:
+            continue
+        seqs = [SequenceSpec(s["seq_id"], s["cached_len"], s["new_len"]) for s in c["sequences"]]
+        n = c["n_ranks"]
+        plan = (plan_full_prefill(seqs, n) if c["kind"] == "full" else
+                plan_partial_prefill(seqs, n, [s["rank_cached_counts"] for s in c["sequences"]]))
+        data = [z[f"s{ci}__in{i}"] for i in range(len(seqs))]
+        for r in range(n):
+            for src in ("host", "device"):
+                arrs = data if src == "host" else [torch.from_numpy(a).cuda() for a in data]
+                b = materialize_rank_block(plan, r, arrs)
+                np.testing.assert_array_equal(b.data.cpu().numpy(), z[f"s{ci}__r{r}__data"])
+                np.testing.assert_array_equal(b.positions.cpu().numpy(), z[f"s{ci}__r{r}__pos"])
+                np.testing.assert_array_equal(b.valid.cpu().numpy(), z[f"s{ci}__r{r}__valid"])
+                np.testing.assert_array_equal(b.seq_ids.cpu().numpy(), z[f"s{ci}__r{r}__seq"])
+
+
+@pytest.mark.parametrize("T,n", [(4096, 2), (1000, 4), (8192, 8), (333, 3)])
+def test_device_gather_kernel_bit_exact_d128(rc, T, n):
+    """rcp_shard_gather at kernel geometry (16-byte rows) vs the oracle restatement."""
+    import torch
+
+    from paper_2411_01783_b200.sharding import SequenceSpec, materialize_rank_block, plan_full_prefill
+
+    rng = np.random.default_rng(T)
+    x = rng.standard_normal((T, 2, 128)).astype(np.float32)
+    plan = plan_full_prefill([SequenceSpec(3, 0, T)], n)
+    xd = torch.from_numpy(x).cuda()
+    for r in range(n):
+        b = materialize_rank_block(plan, r, [xd])
+        want = orc.materialize([orc.Seq(3, 0, T)], n, r, [x])
+        np.testing.assert_array_equal(b.data.cpu().numpy(), want.data)
+        np.testing.assert_array_equal(b.positions.cpu().numpy(), want.pos)
+        np.testing.assert_array_equal(b.valid.cpu().numpy(), want.valid)
+        np.testing.assert_array_equal(b.seq_ids.cpu().numpy(), want.seq)
+        p32, s32 = b.meta32("q")
+        assert np.array_equal(p32.cpu().numpy(), np.where(want.valid, want.pos, -1))
+
+
+def _ring_inputs(rc, name):
+    import torch
+
+    from paper_2411_01783_b200.kv_cache import RankKvCache
+    from paper_2411_01783_b200.sharding import SequenceSpec, materialize_rank_block, plan_full_prefill
+
+    z = G.npz("ring.npz")
+    meta = [int(x) for x in z[f"{name}__meta"]]
+    n, hq, hkv, lens = meta[0], meta[1], meta[2], meta[3:]
+    plan = plan_full_prefill([SequenceSpec(i, 0, t) for i, t in enumerate(lens)], n)
+    cfg = rc.GqaConfig(hq, hkv, 128)
+    dev = lambda a: torch.from_numpy(a).cuda().to(torch.bfloat16)
+    qd = [dev(z[f"{name}__q{i}"]) for i in range(len(lens))]
+    kd = [dev(z[f"{name}__k{i}"]) for i in range(len(lens))]
+    vd = [dev(z[f"{name}__v{i}"]) for i in range(len(lens))]
+    qb = [materialize_rank_block(plan, r, qd) for r in range(n)]
+    kb = [materialize_rank_block(plan, r, kd) for r in range(n)]
+    vb = [materialize_rank_block(plan, r, vd) for r in range(n)]
+    caches = lambda: [RankKvCache(hkv, 128, capacity_tokens=256) for _ in range(n)]
+    return z, n, plan, cfg, qb, kb, vb, caches
+
+
+@pytest.mark.parametrize("name", ["ring_n2_t256", "ring_n3_fused", "ring_n4_t512"])
+def test_ring_prefill_matches_reference_composition(rc, name):
+    from paper_2411_01783_b200.ring import StepTrace, ring_pass_kv_prefill, ring_pass_q_prefill
+
+    z, n, plan, cfg, qb, kb, vb, caches = _ring_inputs(rc, name)
+    tr = StepTrace()
+    kv = ring_pass_kv_prefill(plan, caches(), qb, kb, vb, cfg, trace=tr)
+    pq = ring_pass_q_prefill(plan, caches(), qb, kb, vb, cfg)
+    for r in range(n):
+        o = kv[r].output.data.cpu().numpy()
+        l = kv[r].lse.cpu().numpy()
+        assert np.abs(o - z[f"{name}__r{r}__out"]).max() <= G.O_TOL
+        assert G.lse_err(l, z[f"{name}__r{r}__lse"]) <= G.LSE_TOL
+        # protocol equivalence: pass-KV and pass-Q bit-identical
+        assert np.array_equal(o, pq[r].output.data.cpu().numpy())
+        assert np.array_equal(l, pq[r].lse.cpu().numpy())
+    # message-count law: N-1 KV sends per rank, equal sizes within a step
+    assert len(tr.records) == n * (n - 1)
+    assert len({rec[3] for rec in tr.records}) == 1
+
+
+def test_partial_prefill_and_decode_vs_oracle(rc):
+    """Multi-turn: full prefill -> 5 decode steps -> partial prefill, vs the
+    composed oracle."""
+    import torch
+
+    from paper_2411_01783_b200.kv_cache import RankKvCache
+    from paper_2411_01783_b200.ring import ring_pass_kv_prefill, ring_pass_q_decode, ring_pass_q_prefill
+    from paper_2411_01783_b200.sharding import (SequenceSpec, materialize_rank_block, plan_decode,
+                                                plan_full_prefill, plan_partial_prefill)
+
+    rng = np.random.default_rng(21)
+    n, hq, hkv = 3, 8, 2
+    cfg = rc.GqaConfig(hq, hkv, 128)
+    bf = lambda a: _bf16(a)
+    batch = [4, 9]
+    T0 = [300, 170]
+    caches_g = [RankKvCache(hkv, 128, capacity_tokens=128) for _ in range(n)]
+    caches_o = [orc.Cache(hkv, 128) for _ in range(n)]
+    # turn 1: full prefill
+    seqs = [SequenceSpec(s, 0, t) for s, t in zip(batch, T0)]
+    q = [bf(rng.standard_normal((t, hq, 128))) for t in T0]
+    k = [bf(rng.standard_normal((t, hkv, 128))) for t in T0]
+    v = [bf(rng.standard_normal((t, hkv, 128))) for t in T0]
+    plan = plan_full_prefill(seqs, n)
+    dev = lambda a: torch.from_numpy(a).cuda().to(torch.bfloat16)
+    qb = [materialize_rank_block(plan, r, [dev(x) for x in q]) for r in range(n)]
+    kb = [materialize_rank_block(plan, r, [dev(x) for x in k]) for r in range(n)]
+    vb = [materialize_rank_block(plan, r, [dev(x) for x in v]) for r in range(n)]
+    got = ring_pass_kv_prefill(plan, caches_g, qb, kb, vb, cfg)
+    oseqs = [orc.Seq(s, 0, t) for s, t in zip(batch, T0)]
+    _, want = orc.ring_prefill(oseqs, [[0] * n for _ in oseqs], n, caches_o, q, k, v, hkv)
+    for r in range(n):
+        assert np.abs(got[r].output.data.cpu().numpy() - want[r][0]).max() <= G.O_TOL
+        assert G.lse_err(got[r].lse.cpu().numpy(), want[r][1]) <= G.LSE_TOL
+    # turn 2: decode steps
+    lens = list(T0)
+    for it in range(5):
+        dp = plan_decode(batch, n, it)
+        qt = bf(rng.standard_normal((len(batch), hq, 128)))
+        kt = bf(rng.standard_normal((len(batch), hkv, 128)))
+        vt = bf(rng.standard_normal((len(batch), hkv, 128)))
+        pos = list(lens)
+        o, l = ring_pass_q_decode(dp, caches_g, dev(qt), dev(kt), dev(vt), pos, cfg)
+        wo = orc.ring_decode(batch, n, it, caches_o, qt, kt, vt, pos, hkv)
+        for b in range(len(batch)):
+            assert np.abs(o[b].cpu().numpy() - wo[b][0][0]).max() <= G.O_TOL
+            assert G.lse_err(l[b].cpu().numpy(), wo[b][1][0]) <= G.LSE_TOL
+        lens = [x + 1 for x in lens]
+    # turn 3: partial prefill (new tokens continue after the cached history)
+    T1 = [40, 23]
+    layout = [[caches_g[r].cached_len(s) for r in range(n)] for s in batch]
+    seqs = [SequenceSpec(s, P, t) for s, P, t in zip(batch, lens, T1)]
+    plan = plan_partial_prefill(seqs, n, layout)
+    q = [bf(rng.standard_normal((t, hq, 128))) for t in T1]
+    k = [bf(rng.standard_normal((t, hkv, 128))) for t in T1]
+    v = [bf(rng.standard_normal((t, hkv, 128))) for t in T1]
+    qb = [materialize_rank_block(plan, r, [dev(x) for x in q]) for r in range(n)]
+    kb = [materialize_rank_block(plan, r, [dev(x) for x in k]) for r in range(n)]
+    vb = [materialize_rank_block(plan, r, [dev(x) for x in v]) for r in range(n)]
+    import copy
+    caches_g2 = caches_g  # pass-Q needs its own caches: rebuild by replay is costly; compare pass-KV here
+    got = ring_pass_kv_prefill(plan, caches_g2, qb, kb, vb, cfg)
+    oseqs = [orc.Seq(s, P, t) for s, P, t in zip(batch, lens, T1)]
+    _, want = orc.ring_prefill(oseqs, layout, n, caches_o, q, k, v, hkv)
+    for r in range(n):
+        assert np.abs(got[r].output.data.cpu().numpy() - want[r][0]).max() <= G.O_TOL
+        assert G.lse_err(got[r].lse.cpu().numpy(), want[r][1]) <= G.LSE_TOL
+
+
+def _bf16(x):
+    x = np.asarray(x, np.float32)
+    u = x.view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32)
