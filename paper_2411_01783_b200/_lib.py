@@ -57,9 +57,9 @@ SIGNATURES = {
 
 _lib = None
 
-# Kernel launches issued through this binding (per C-ABI call: rcp_attn_fwd 3 =
-# two tile summaries + attention; rcp_decode_attn 2; every other call 1).
-LAUNCHES_PER_CALL = {"rcp_attn_fwd": 3, "rcp_decode_attn": 2}
+# Kernel launches issued through this binding (per C-ABI call: rcp_attn_fwd 4 =
+# two tile summaries + active lists + attention; rcp_decode_attn 2; others 1).
+LAUNCHES_PER_CALL = {"rcp_attn_fwd": 4, "rcp_decode_attn": 2}
 launch_count = 0
 
 

@@ -2,30 +2,36 @@
 //
 // Replaces ringcp.attention.gqa_attention (attention.py:230-282) on the ring
 // hot path.  One CTA = two 128-row query tiles of one query head; the tiles
-// share every K/V tile the TMA producer streams through a 2-stage ring.
+// share every 64-key K/V block the TMA producer streams through an 8-slot ring.
 //
 // Warp roles (384 threads):
 //   warp 0      TMA producer (one elected lane): Q once, then K_j / V_j
-//   warp 1      MMA issuer (one elected lane):   S_t = Q_t K_j^T  (SS, K-major)
-//                                                O_t += P_t V_j   (TS, P in TMEM)
-//   warp 2      TMEM allocator (512 columns: S0 | S1 | O0 | O1)
+//   warp 1      MMA issuer (one elected lane):   S_t(j) = Q_t K_j^T   (SS, K-major)
+//                                                O_t   += P_t(j) V_j  (TS, P in TMEM)
+//   warp 2      TMEM allocator
 //   warps 4-7   softmax for query tile 0 (thread i owns TMEM lane / row i)
 //   warps 8-11  softmax for query tile 1
-// The MMA order S0(j) S1(j) | PV0(j) S0(j+1) PV1(j) S1(j+1) | ... lets softmax of
-// one tile overlap the tensor-core work of the other ("ping-pong").  P_t is
-// written as packed bf16 into the first 64 columns of S_t's TMEM region and
-// consumed from TMEM by the TS MMA.  tcgen05 ops complete in issue order, so
-// the commit that publishes S_t(j) also proves PV_t(j-1) finished — the softmax
-// may then rescale O_t in place without another barrier.
 //
-// Masking: per-tile summaries (min/max position and sequence over valid rows)
-// classify every (query tile, key tile) pair as EMPTY (skipped: no TMA, no MMA),
-// FULL (no per-element mask) or PARTIAL (per-element seq/pos test), which keeps
-// the general position-based mask of the reference off the dense path.
-// Softmax runs in the exp2 domain with a lazily raised running max (rescale O
-// only when the max grows by more than 2^8); LSE = (m + log2 l) * ln 2 (natural
-// log, as attention.py:274-277) and rows that admit nothing give 0 / -inf.
+// TMEM (512 columns): O0 [0,128) | O1 [128,256) | S0 buffers [256,320) [320,384)
+// | S1 buffers [384,448) [448,512).  S is double-buffered per query tile and
+// P(j) (packed bf16) is written over the first 32 columns of the buffer S(j)
+// came from.  The MMA warp issues S_t(j+2) into a buffer right after PV_t(j)
+// (tcgen05 ops complete in issue order), so while the softmax works on block j
+// the tensor cores already hold S(j+1): the softmax never waits for a PV->S
+// round trip and both pipes stay busy.  The (rare) in-place rescale of O waits
+// for a per-tile "PV done" barrier first.
+//
+// Masking: per-tile summaries (min/max position and sequence over valid rows,
+// 128-row query tiles, 64-row key blocks) classify every (query tile, key
+// block) pair as EMPTY (skipped: no TMA, no MMA), FULL (no per-element mask) or
+// PARTIAL (per-element seq/pos test), which keeps the general position-based
+// mask of the reference off the dense path.  Softmax runs in the exp2 domain
+// with a lazily raised running max (rescale only when it grows by > 2^8), part
+// of the exp2 on the FMA pipe (cubic polynomial) to relieve MUFU; LSE =
+// (m + log2 l) * ln 2 (natural log, attention.py:274-277); rows that admit
+// nothing give O = 0, LSE = -inf.
 #include <climits>
+#include <cstring>
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -34,13 +40,20 @@
 namespace rcp {
 
 constexpr int kD = 128;
-constexpr int kTileRows = 128;
-constexpr int kStages = 2;
+constexpr int kQRows = 128;        // query tile rows (MMA M)
+constexpr int kKRows = 64;         // key block rows  (MMA N of S, K of PV)
+constexpr int kSlots = 8;          // unified K/V TMA ring (K_j, V_j, K_j+1, ...)
 constexpr int kThreads = 384;
-constexpr uint32_t kTileBytes = kTileRows * kD * 2;  // 32 KB: two 16 KB SW128 boxes
-constexpr uint32_t kBoxBytes = kTileBytes / 2;
-constexpr uint32_t kSmemBytes = (2 + 2 * kStages) * kTileBytes + 1024;
+constexpr uint32_t kQTileBytes = kQRows * kD * 2;   // 32 KB: two 16 KB SW128 boxes
+constexpr uint32_t kQBoxBytes = kQTileBytes / 2;
+constexpr uint32_t kKVBytes = kKRows * kD * 2;      // 16 KB: two 8 KB SW128 boxes
+constexpr uint32_t kKVBoxBytes = kKVBytes / 2;
+constexpr uint32_t kSmemBytes = 2 * kQTileBytes + kSlots * kKVBytes + 1024;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+// Of every 8 score pairs of a FULL block, this many take exp2 on the FMA pipe
+// (cubic polynomial) instead of MUFU.EX2, balancing the two pipes.
+constexpr int kPolyPairsPer8 = 2;
+constexpr uint32_t kTmemO = 0, kTmemS = 256;  // column bases
 
 struct AttnParams {
   CUtensorMap tm_q, tm_k, tm_v;
@@ -48,15 +61,29 @@ struct AttnParams {
   const int32_t* q_seq;
   const int32_t* k_pos;
   const int32_t* k_seq;
-  const TileSum* q_sum;
-  const TileSum* k_sum;
+  const TileSum* q_sum;  // per 128-row query tile
+  const TileSum* k_sum;  // per 64-row key block
+  const uint32_t* act;   // per query-tile pair: active key blocks, j | cls0 << 24 | cls1 << 26
+  const int* act_n;      // per query-tile pair: number of active key blocks
   float* o;
   float* lse;
   int tq, tk, hq, hkv, group;
-  int n_qtiles, n_qblk, n_ktiles;
+  int n_qtiles, n_qblk, n_kblocks;
   int mode;
   float scale_log2;
+  long long* trace;  // RCP_TRACE builds only: per-CTA role timestamps (clock64)
 };
+
+#ifndef RCP_TRACE
+#define RCP_TRACE 0
+#endif
+// Trace layout: CTA b < kTraceCtas, iteration it < kTraceIters, event e < kTraceEv.
+constexpr int kTraceCtas = 8, kTraceIters = 64, kTraceEv = 16;
+#define TRACE(e, it)                                                                    \
+  do {                                                                                  \
+    if (RCP_TRACE && p.trace && blockIdx.x < kTraceCtas && (it) < kTraceIters)          \
+      p.trace[(blockIdx.x * kTraceIters + (it)) * kTraceEv + (e)] = clock64();          \
+  } while (0)
 
 __device__ __forceinline__ TileSum load_sum(const TileSum* p, int i, int n) {
   TileSum t;
@@ -72,59 +99,137 @@ __device__ __forceinline__ TileSum load_sum(const TileSum* p, int i, int n) {
   return t;
 }
 
-// Next key tile after j that is non-empty for either query tile (-1: done).
-__device__ __forceinline__ int next_active(const AttnParams& p, int j, const TileSum& q0,
-                                           const TileSum& q1) {
-  for (++j; j < p.n_ktiles; ++j) {
-    const TileSum k = load_sum(p.k_sum, j, p.n_ktiles);
-    if (classify_tile(q0, k) != kTileEmpty || classify_tile(q1, k) != kTileEmpty) return j;
+// Active-list entry: key block index and the class of the pair with each query tile.
+__device__ __forceinline__ int act_j(uint32_t e) { return static_cast<int>(e & 0xFFFFFFu); }
+__device__ __forceinline__ int act_cls(uint32_t e, int t) { return static_cast<int>((e >> (24 + 2 * t)) & 3u); }
+
+// Pre-pass: for every query-tile pair (one CTA of 256 threads each), the
+// ascending list of key blocks that are non-empty for either tile, with both
+// classes, compacted with a block-wide ballot scan.
+__global__ void __launch_bounds__(256) active_list_kernel(const TileSum* __restrict__ q_sum,
+                                                          const TileSum* __restrict__ k_sum,
+                                                          int n_qtiles, int n_kblocks,
+                                                          uint32_t* __restrict__ act,
+                                                          int* __restrict__ act_n) {
+  __shared__ int warp_cnt[8];
+  __shared__ int base;
+  const int qb = blockIdx.x;
+  const TileSum q0 = load_sum(q_sum, 2 * qb, n_qtiles), q1 = load_sum(q_sum, 2 * qb + 1, n_qtiles);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  uint32_t* out = act + static_cast<int64_t>(qb) * n_kblocks;
+  for (int j0 = 0; j0 < n_kblocks; j0 += 256) {
+    const int j = j0 + threadIdx.x;
+    uint32_t e = 0;
+    bool on = false;
+    if (j < n_kblocks) {
+      const TileSum k = load_sum(k_sum, j, n_kblocks);
+      const int c0 = classify_tile(q0, k), c1 = classify_tile(q1, k);
+      on = (c0 | c1) != kTileEmpty;
+      e = static_cast<uint32_t>(j) | (static_cast<uint32_t>(c0) << 24) | (static_cast<uint32_t>(c1) << 26);
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) warp_cnt[wid] = __popc(bal);
+    __syncthreads();
+    int off = base;
+    for (int w2 = 0; w2 < wid; ++w2) off += warp_cnt[w2];
+    if (on) out[off + __popc(bal & ((1u << lane) - 1u))] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w2 = 0; w2 < 8; ++w2) tot += warp_cnt[w2];
+      base += tot;
+    }
+    __syncthreads();
   }
-  return -1;
+  if (threadIdx.x == 0) act_n[qb] = base;
 }
 
-__device__ __forceinline__ uint64_t kmajor_desc(uint32_t tile_addr, int kk) {
-  // K-major SW128: 8-row groups 1024 B apart; k-step kk (16 elements) selects
-  // box kk/4 and a 32-byte column offset inside the 128-byte swizzle row.
-  return make_sw128_desc(tile_addr + (kk >> 2) * kBoxBytes + (kk & 3) * 32, 16, 1024);
+// K-major SW128 operand (Q or K): 8-row groups 1024 B apart; k-step kk (16
+// elements of D) selects box kk/4 and a 32-byte offset in the 128-byte row.
+__device__ __forceinline__ uint64_t kmajor_desc(uint32_t tile_addr, uint32_t box_bytes, int kk) {
+  return make_sw128_desc(tile_addr + (kk >> 2) * box_bytes + (kk & 3) * 32, 16, 1024);
 }
-__device__ __forceinline__ uint64_t mnmajor_desc(uint32_t tile_addr, int kk) {
-  // MN-major SW128 (V as B operand, N = head dim contiguous): the two 64-column
-  // boxes are LBO = 16 KB apart, 8-key groups SBO = 1 KB; k-step = 16 keys.
-  return make_sw128_desc(tile_addr + kk * 2048, kBoxBytes, 1024);
+// MN-major SW128 V block as the B operand (N = head dim contiguous): the two
+// 64-column boxes are LBO = 8 KB apart, 8-key groups SBO = 1 KB; k-step = 16 keys.
+__device__ __forceinline__ uint64_t v_desc(uint32_t tile_addr, int kk) {
+  return make_sw128_desc(tile_addr + kk * 2048, kKVBoxBytes, 1024);
+}
+
+// ---- packed fp32x2 (FFMA2 / FADD2) and the FMA-pipe exp2
+__device__ __forceinline__ uint64_t f2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 unf2(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// 2^x for finite x <= 8 on the FMA/ALU pipes: round-to-nearest split x = n + f,
+// f in [-1/2, 1/2], cubic minimax for 2^f (max rel. error 1.0e-4, far below the
+// bf16 rounding of P), exponent add.  x is clamped at -126 (result >= 2^-126).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.0f);
+  const float t = __fadd_rn(x, 12582912.0f);  // 1.5 * 2^23: low mantissa bits = round(x)
+  const float f = __fsub_rn(x, __fsub_rn(t, 12582912.0f));
+  const float p = fmaf(fmaf(fmaf(0.05500893f, f, 0.24221097f), f, 0.69328290f), f, 1.0f);
+  // (bits(t) << 23) == round(x) << 23 modulo 2^32 because 0x4B400000 << 23 == 0
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
 __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                        // 2 tiles
-  uint8_t* sK = smem + 2 * kTileBytes;       // kStages tiles
-  uint8_t* sV = sK + kStages * kTileBytes;   // kStages tiles
+  uint8_t* sQ = smem;                         // 2 query tiles
+  uint8_t* sKV = smem + 2 * kQTileBytes;      // kSlots K/V blocks
 
-  __shared__ uint64_t bar_q, bar_kf[kStages], bar_ke[kStages], bar_vf[kStages], bar_ve[kStages];
-  __shared__ uint64_t bar_s[2], bar_p[2], bar_o[2];
+  __shared__ uint64_t bar_q, bar_full[kSlots], bar_empty[kSlots];
+  __shared__ uint64_t bar_s[2][2], bar_p[2][2], bar_pv[2], bar_o[2];
   __shared__ uint32_t tmem_slot;
 
   const int warp = static_cast<int>(warp_id());
   const int head = blockIdx.x % p.hq;
   const int qblk = p.n_qblk - 1 - static_cast<int>(blockIdx.x / p.hq);  // late (heavy) blocks first
   const int kvh = head / p.group;
-  const TileSum qs0 = load_sum(p.q_sum, 2 * qblk, p.n_qtiles);
-  const TileSum qs1 = load_sum(p.q_sum, 2 * qblk + 1, p.n_qtiles);
-
   if (threadIdx.x == 0) {
     mbar_init(&bar_q, 1);
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&bar_kf[s], 1);
-      mbar_init(&bar_ke[s], 1);
-      mbar_init(&bar_vf[s], 1);
-      mbar_init(&bar_ve[s], 1);
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(&bar_full[s], 1);
+      mbar_init(&bar_empty[s], 1);
     }
     for (int t = 0; t < 2; ++t) {
-      mbar_init(&bar_s[t], 1);
-      mbar_init(&bar_p[t], 128);
+      mbar_init(&bar_s[t][0], 1);
+      mbar_init(&bar_s[t][1], 1);
+      mbar_init(&bar_p[t][0], 128);
+      mbar_init(&bar_p[t][1], 128);
+      mbar_init(&bar_pv[t], 1);
       mbar_init(&bar_o[t], 1);
     }
+#ifdef RCP_TRACE_BUILD
+    if (blockIdx.x == 0 && p.trace) {
+      p.trace[kTraceCtas * kTraceIters * kTraceEv + 0] = smem_u32(&bar_q);
+      p.trace[kTraceCtas * kTraceIters * kTraceEv + 1] = smem_u32(&bar_full[0]);
+      p.trace[kTraceCtas * kTraceIters * kTraceEv + 2] = smem_u32(&bar_empty[0]);
+      p.trace[kTraceCtas * kTraceIters * kTraceEv + 3] = smem_u32(&bar_s[0][0]);
+      p.trace[kTraceCtas * kTraceIters * kTraceEv + 4] = smem_u32(&bar_p[0][0]);
+      p.trace[kTraceCtas * kTraceIters * kTraceEv + 5] = smem_u32(&bar_pv[0]);
+      p.trace[kTraceCtas * kTraceIters * kTraceEv + 6] = smem_u32(&bar_o[0]);
+    }
+#endif
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(&tmem_slot);
@@ -139,28 +244,32 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       tma_prefetch_desc(&p.tm_q);
       tma_prefetch_desc(&p.tm_k);
       tma_prefetch_desc(&p.tm_v);
-      int j = next_active(p, -1, qs0, qs1);
-      if (j >= 0) {
+      const int n = __ldg(p.act_n + qblk);
+      const uint32_t* act = p.act + static_cast<int64_t>(qblk) * p.n_kblocks;
+      if (n > 0) {
         const uint64_t pol_q = policy_evict_first();
         const uint64_t pol_kv = policy_evict_last();
-        mbar_arrive_expect_tx(&bar_q, 2 * kTileBytes);
+        mbar_arrive_expect_tx(&bar_q, 2 * kQTileBytes);
         for (int t = 0; t < 2; ++t)
           for (int h = 0; h < 2; ++h)
-            tma_load_2d(sQ + t * kTileBytes + h * kBoxBytes, &p.tm_q, &bar_q, head * kD + h * 64,
-                        (2 * qblk + t) * kTileRows, pol_q);
-        for (int it = 0; j >= 0; j = next_active(p, j, qs0, qs1), ++it) {
-          const int s = it % kStages;
-          const uint32_t ph = (it / kStages) & 1;
-          mbar_wait(&bar_ke[s], ph ^ 1);
-          mbar_arrive_expect_tx(&bar_kf[s], kTileBytes);
-          for (int h = 0; h < 2; ++h)
-            tma_load_2d(sK + s * kTileBytes + h * kBoxBytes, &p.tm_k, &bar_kf[s],
-                        kvh * kD + h * 64, j * kTileRows, pol_kv);
-          mbar_wait(&bar_ve[s], ph ^ 1);
-          mbar_arrive_expect_tx(&bar_vf[s], kTileBytes);
-          for (int h = 0; h < 2; ++h)
-            tma_load_2d(sV + s * kTileBytes + h * kBoxBytes, &p.tm_v, &bar_vf[s],
-                        kvh * kD + h * 64, j * kTileRows, pol_kv);
+            tma_load_2d(sQ + t * kQTileBytes + h * kQBoxBytes, &p.tm_q, &bar_q, head * kD + h * 64,
+                        (2 * qblk + t) * kQRows, pol_q);
+        uint32_t ld = 0;  // load counter: K_j is load 2*it, V_j load 2*it + 1
+        uint32_t e_next = __ldg(act);
+        for (int it = 0; it < n; ++it) {
+          const int j = act_j(e_next);
+          if (it + 1 < n) e_next = __ldg(act + it + 1);
+#pragma unroll
+          for (int kv = 0; kv < 2; ++kv, ++ld) {
+            const uint32_t slot = ld % kSlots, ph = (ld / kSlots) & 1;
+            mbar_wait(&bar_empty[slot], ph ^ 1);
+            TRACE(6 + kv, ld / 2);
+            mbar_arrive_expect_tx(&bar_full[slot], kKVBytes);
+            const CUtensorMap* map = kv ? &p.tm_v : &p.tm_k;
+            for (int h = 0; h < 2; ++h)
+              tma_load_2d(sKV + slot * kKVBytes + h * kKVBoxBytes, map, &bar_full[slot],
+                          kvh * kD + h * 64, j * kKRows, pol_kv);
+          }
         }
       }
     }
@@ -168,102 +277,125 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (elect_one()) {
-      const uint32_t idesc_s = make_idesc_bf16_f32(128, 128, 0, 0);
-      const uint32_t idesc_o = make_idesc_bf16_f32(128, 128, 0, 1);
-      const uint32_t q_addr = smem_u32(sQ), k_addr = smem_u32(sK), v_addr = smem_u32(sV);
-      auto issue_s = [&](int t, int stage) {
-        const uint32_t qa = q_addr + t * kTileBytes, ka = k_addr + stage * kTileBytes;
+      const uint32_t idesc_s = make_idesc_bf16_f32(kQRows, kKRows, 0, 0);
+      const uint32_t idesc_o = make_idesc_bf16_f32(kQRows, kD, 0, 1);
+      auto wait_load = [&](uint32_t ld) {
+        mbar_wait(&bar_full[ld % kSlots], (ld / kSlots) & 1);
+        tc_fence_after();
+      };
+      const uint32_t q_base = smem_u32(sQ), kv_base = smem_u32(sKV);
+      auto issue_s = [&](int t, int buf, uint32_t ld) {
+        const uint32_t qa = q_base + t * kQTileBytes, ka = kv_base + (ld % kSlots) * kKVBytes;
+        const uint32_t d = tmem + kTmemS + (2 * t + buf) * kKRows;
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk)
-          mma_ss(tmem + t * 128, kmajor_desc(qa, kk), kmajor_desc(ka, kk), idesc_s, kk > 0);
+          mma_ss(d, kmajor_desc(qa, kQBoxBytes, kk), kmajor_desc(ka, kKVBoxBytes, kk), idesc_s,
+                 kk > 0);
       };
-      auto issue_pv = [&](int t, int stage, bool acc) {
-        const uint32_t va = v_addr + stage * kTileBytes;
+      auto issue_pv = [&](int t, int buf, uint32_t ld, bool acc) {
+        const uint32_t va = kv_base + (ld % kSlots) * kKVBytes;
+        const uint32_t pa = tmem + kTmemS + (2 * t + buf) * kKRows;
 #pragma unroll
-        for (int kk = 0; kk < kTileRows / 16; ++kk)
-          mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmajor_desc(va, kk), idesc_o,
+        for (int kk = 0; kk < kKRows / 16; ++kk)
+          mma_ts(tmem + kTmemO + t * kD, pa + kk * 8, v_desc(va, kk), idesc_o,
                  (acc || kk > 0) ? 1u : 0u);
       };
-      int j = next_active(p, -1, qs0, qs1);
-      if (j >= 0) {
+      const int n = __ldg(p.act_n + qblk);
+      if (n > 0) {
         mbar_wait(&bar_q, 0);
-        mbar_wait(&bar_kf[0], 0);
-        tc_fence_after();
-        issue_s(0, 0);
-        mma_commit(&bar_s[0]);
-        issue_s(1, 0);
-        mma_commit(&bar_s[1]);
-        mma_commit(&bar_ke[0]);
-        for (int it = 0;; ++it) {
-          const int jn = next_active(p, j, qs0, qs1);
-          const int s = it % kStages;
-          const int s1 = (it + 1) % kStages;
-          const uint32_t ph1 = ((it + 1) / kStages) & 1;
-          mbar_wait(&bar_vf[s], (it / kStages) & 1);
-          mbar_wait(&bar_p[0], it & 1);
+        // prologue: S(0) and S(1) for both tiles
+        wait_load(0);
+        issue_s(0, 0, 0);
+        mma_commit(&bar_s[0][0]);
+        issue_s(1, 0, 0);
+        mma_commit(&bar_s[1][0]);
+        mma_commit(&bar_empty[0]);
+        if (n > 1) {
+          wait_load(2);
+          issue_s(0, 1, 2);
+          mma_commit(&bar_s[0][1]);
+          issue_s(1, 1, 2);
+          mma_commit(&bar_s[1][1]);
+          mma_commit(&bar_empty[2 % kSlots]);
+        }
+        for (int it = 0; it < n; ++it) {
+          const int buf = it & 1;
+          const bool last = it + 1 == n, has2 = it + 2 < n;
+          const uint32_t ldv = 2 * it + 1, ldk2 = 2 * it + 4;
+          wait_load(ldv);
+          TRACE(12, it);
+          // tile 0: PV0(it) then, into the same buffer, S0(it+2)
+          mbar_wait(&bar_p[0][buf], (it >> 1) & 1);
           tc_fence_after();
-          issue_pv(0, s, it > 0);
-          if (jn >= 0) {
-            mbar_wait(&bar_kf[s1], ph1);
-            tc_fence_after();
-            issue_s(0, s1);
-            mma_commit(&bar_s[0]);
-          } else {
-            mma_commit(&bar_o[0]);
+          TRACE(0, it);
+          issue_pv(0, buf, ldv, it > 0);
+          mma_commit(last ? &bar_o[0] : &bar_pv[0]);
+          if (has2) {
+            wait_load(ldk2);
+            issue_s(0, buf, ldk2);
+            mma_commit(&bar_s[0][buf]);
           }
-          mbar_wait(&bar_p[1], it & 1);
+          // tile 1
+          mbar_wait(&bar_p[1][buf], (it >> 1) & 1);
           tc_fence_after();
-          issue_pv(1, s, it > 0);
-          mma_commit(&bar_ve[s]);
-          if (jn >= 0) {
-            issue_s(1, s1);
-            mma_commit(&bar_s[1]);
-            mma_commit(&bar_ke[s1]);
-          } else {
-            mma_commit(&bar_o[1]);
-            break;
+          TRACE(1, it);
+          issue_pv(1, buf, ldv, it > 0);
+          mma_commit(last ? &bar_o[1] : &bar_pv[1]);
+          mma_commit(&bar_empty[ldv % kSlots]);
+          TRACE(13, it);
+          if (has2) {
+            issue_s(1, buf, ldk2);
+            mma_commit(&bar_s[1][buf]);
+            mma_commit(&bar_empty[ldk2 % kSlots]);
           }
-          j = jn;
+          TRACE(14, it);
         }
       }
     }
     __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax + epilogue
-    const int w = (warp - 4) >> 2;                  // query tile 0 / 1
+    const int w = (warp - 4) >> 2;                                 // query tile 0 / 1
     const int t = static_cast<int>(threadIdx.x) - 128 - 128 * w;  // row inside the tile
-    const int row = (2 * qblk + w) * kTileRows + t;
-    const TileSum& qs = w ? qs1 : qs0;
+    const int row = (2 * qblk + w) * kQRows + t;
     const bool row_ok = row < p.tq;
     const int my_pos = row_ok ? __ldg(p.q_pos + row) : -1;
     const int my_seq = row_ok ? __ldg(p.q_seq + row) : RCP_SEQ_PAD_Q;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
-    const uint32_t s_addr = lane_base + w * 128;
-    const uint32_t o_addr = lane_base + 256 + w * 128;
+    const uint32_t o_addr = lane_base + kTmemO + w * kD;
     const float sl2 = p.scale_log2;
+    const uint64_t sl2x2 = f2(sl2, sl2);
     float m = -INFINITY, l = 0.f;
+    const int n = __ldg(p.act_n + qblk);
+    const uint32_t* act = p.act + static_cast<int64_t>(qblk) * p.n_kblocks;
+    uint32_t e_next = n > 0 ? __ldg(act) : 0u;
     int it = 0;
-    for (int j = next_active(p, -1, qs0, qs1); j >= 0; j = next_active(p, j, qs0, qs1), ++it) {
-      const TileSum ks = load_sum(p.k_sum, j, p.n_ktiles);
-      const int cls = classify_tile(qs, ks);
-      mbar_wait(&bar_s[w], it & 1);
+    for (; it < n; ++it) {
+      const int buf = it & 1;
+      const uint32_t s_addr = lane_base + kTmemS + (2 * w + buf) * kKRows;
+      const uint32_t e = e_next;
+      if (it + 1 < n) e_next = __ldg(act + it + 1);
+      const int j = act_j(e);
+      const int cls = act_cls(e, w);
+      mbar_wait(&bar_s[w][buf], (it >> 1) & 1);
       tc_fence_after();
-      uint32_t pk[64];
-      if (cls != kTileEmpty) {
-        uint32_t sr[128];
-#pragma unroll
-        for (int c = 0; c < 128; c += 32) tmem_ld32(s_addr + c, sr + c);
+      if (t == 0) TRACE(2 + 2 * w, it);
+      if (cls != kTileEmpty) {  // warp-uniform
+        uint32_t sr[64];
+        tmem_ld32(s_addr, sr);
+        tmem_ld32(s_addr + 32, sr + 32);
         tmem_ld_wait();
-        float s[128];
+        float s[64];
 #pragma unroll
-        for (int c = 0; c < 128; ++c) s[c] = __uint_as_float(sr[c]);
+        for (int c = 0; c < 64; ++c) s[c] = __uint_as_float(sr[c]);
+        if (t == 0 && w == 0) TRACE(8, it);
         if (cls == kTilePartial) {
-          const int base = j * kTileRows;
-          if (base + kTileRows <= p.tk) {
+          const int base = j * kKRows;
+          if (base + kKRows <= p.tk) {
             const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + base);
             const int4* ks4 = reinterpret_cast<const int4*>(p.k_seq + base);
 #pragma unroll
-            for (int c4 = 0; c4 < 32; ++c4) {
+            for (int c4 = 0; c4 < 16; ++c4) {
               const int4 kp = __ldg(kp4 + c4), kq = __ldg(ks4 + c4);
               if (!(kq.x == my_seq && kp.x <= my_pos)) s[4 * c4 + 0] = -INFINITY;
               if (!(kq.y == my_seq && kp.y <= my_pos)) s[4 * c4 + 1] = -INFINITY;
@@ -272,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             }
           } else {
 #pragma unroll
-            for (int c = 0; c < 128; ++c) {
+            for (int c = 0; c < 64; ++c) {
               const int kidx = base + c;
               const bool ok = kidx < p.tk && __ldg(p.k_seq + kidx) == my_seq &&
                               __ldg(p.k_pos + kidx) <= my_pos;
@@ -280,9 +412,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             }
           }
         }
-        float mx = s[0];
+        float m8[8];
 #pragma unroll
-        for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
+        for (int k = 0; k < 8; ++k) m8[k] = s[k];
+#pragma unroll
+        for (int c = 8; c < 64; c += 8)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m8[k] = fmaxf(m8[k], s[c + k]);
+        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
         const float m_old = m;
         const float m_new = fmaxf(m, mx * sl2);
         const bool need = m_new > m + kRescaleThreshold;  // also true for -inf -> finite
@@ -291,22 +429,47 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         // -inf, so exp2(s - 0) = 0.  Everything below is warp-uniform (the
         // tcgen05.ld/st are .sync.aligned).
         const float m_use = (m == -INFINITY) ? 0.f : m;
-        float sum = 0.f;
+        const uint64_t negm2 = f2(-m_use, -m_use);
+        if (t == 0 && w == 0) TRACE(9, it);
+        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+        uint32_t pk[32];
+        if (cls == kTileFull) {
 #pragma unroll
-        for (int c = 0; c < 128; c += 2) {
-          const float p0 = ex2_approx(fmaf(s[c], sl2, -m_use));
-          const float p1 = ex2_approx(fmaf(s[c + 1], sl2, -m_use));
-          sum += p0 + p1;
-          pk[c >> 1] = pack_bf16x2(p0, p1);
+          for (int i = 0; i < 32; ++i) {
+            const float2 x = unf2(ffma2(f2(s[2 * i], s[2 * i + 1]), sl2x2, negm2));
+            float p0, p1;
+            if ((i & 7) < kPolyPairsPer8) {
+              p0 = ex2_poly(x.x);
+              p1 = ex2_poly(x.y);
+            } else {
+              p0 = ex2_approx(x.x);
+              p1 = ex2_approx(x.y);
+            }
+            acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
+            pk[i] = pack_bf16x2(p0, p1);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float2 x = unf2(ffma2(f2(s[2 * i], s[2 * i + 1]), sl2x2, negm2));
+            const float p0 = ex2_approx(x.x), p1 = ex2_approx(x.y);
+            acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
+            pk[i] = pack_bf16x2(p0, p1);
+          }
         }
+        tmem_st32(s_addr, pk);
+        if (t == 0 && w == 0) TRACE(10, it);
+        const float2 a01 = unf2(fadd2(acc2[0], acc2[1]));
+        const float2 a23 = unf2(fadd2(acc2[2], acc2[3]));
+        const float sum = (a01.x + a01.y) + (a23.x + a23.y);
         const float f = (need && m_old != -INFINITY) ? ex2_approx(m_old - m) : 1.0f;
         l = (m_old == -INFINITY ? 0.f : l * f) + sum;
-        tmem_st32(s_addr, pk);
-        tmem_st32(s_addr + 32, pk + 32);
         if (__any_sync(0xffffffffu, f != 1.0f && it > 0)) {
-          // Rescale O_t rows in place (TMEM); PV_t(it-1) is complete (see header).
+          // Rescale O_t rows in place once PV_t(it-1) has landed in TMEM.
+          mbar_wait(&bar_pv[w], (it - 1) & 1);
+          tc_fence_after();
 #pragma unroll
-          for (int c = 0; c < 128; c += 32) {
+          for (int c = 0; c < kD; c += 32) {
             uint32_t r[32];
             tmem_ld32(o_addr + c, r);
             tmem_ld_wait();
@@ -316,14 +479,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
           }
         }
       } else {
+        uint32_t pk[32];
 #pragma unroll
-        for (int i = 0; i < 64; ++i) pk[i] = 0u;
+        for (int i = 0; i < 32; ++i) pk[i] = 0u;
         tmem_st32(s_addr, pk);
-        tmem_st32(s_addr + 32, pk + 32);
       }
+      if (t == 0 && w == 0) TRACE(11, it);
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&bar_p[w]);
+      if (t == 0) TRACE(3 + 2 * w, it);
+      // One P barrier per S buffer: a warp may run one block ahead of the rest
+      // of its warpgroup (S(it+1) is already computed), so arrivals of
+      // consecutive blocks must not share a barrier phase.
+      mbar_arrive(&bar_p[w][buf]);
     }
 
     // epilogue: O / l, LSE, optional merge into the running (O, LSE)
@@ -339,9 +507,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       float* orow = p.o + (static_cast<int64_t>(row) * p.hq + head) * kD;
       float* lrow = p.lse + static_cast<int64_t>(row) * p.hq + head;
       MergeW mw;
+      mw.lse = lse_new;
+      mw.wa = 0.f;
+      mw.wb = 1.f;
       if (merge && row_ok) mw = merge_weights(__ldg(lrow), lse_new);
 #pragma unroll
-      for (int c = 0; c < 128; c += 32) {
+      for (int c = 0; c < kD; c += 32) {
         uint32_t r[32];
         if (it > 0) {
           tmem_ld32(o_addr + c, r);
@@ -389,9 +560,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2-D map over a token-major [rows, heads*128] bf16 array; box = 128 rows x 64 cols, SW128.
+// 2-D map over a token-major [rows, heads*128] bf16 array; box = box_rows x 64 cols, SW128.
 static int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols,
-                    int64_t row_stride_elems) {
+                    int64_t row_stride_elems, uint32_t box_rows) {
   auto fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -399,7 +570,7 @@ static int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols
   }
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_stride_elems) * 2};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -416,8 +587,21 @@ static int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols
 
 using namespace rcp;
 
+static long long* g_trace = nullptr;
+// Debug hook (RCP_TRACE builds): device buffer of kTraceCtas*kTraceIters*kTraceEv int64.
+extern "C" void rcp_debug_set_trace(long long* buf) { g_trace = buf; }
+#ifdef RCP_TRACE_BUILD
+// Debug hook: {1 + block, thread, barrier smem address, parity} of the first hung wait.
+extern "C" void rcp_debug_hang_info(int* out) {
+  cudaMemcpyFromSymbol(out, g_hang_info, sizeof(int) * 4);
+}
+#endif
+
+// Workspace: tile summaries | active lists (n_qblk x n_kblocks) | list lengths.
 extern "C" size_t rcp_attn_workspace_bytes(int64_t tq, int64_t tk) {
-  return static_cast<size_t>(((tq + 127) / 128 + (tk + 127) / 128) * sizeof(TileSum));
+  const int64_t nq = (tq + kQRows - 1) / kQRows, nk = (tk + kKRows - 1) / kKRows;
+  const int64_t nqb = (nq + 1) / 2;
+  return static_cast<size_t>((nq + nk) * sizeof(TileSum) + nqb * nk * 4 + nqb * 4 + 256);
 }
 
 extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
@@ -458,15 +642,27 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
   AttnParams prm;
   memset(&prm, 0, sizeof(prm));
   int rc;
-  if ((rc = make_map(&prm.tm_q, q, tq, static_cast<int64_t>(hq) * kD, q_row_stride)) != RCP_OK) return rc;
-  if ((rc = make_map(&prm.tm_k, k, tk, static_cast<int64_t>(hkv) * kD, k_row_stride)) != RCP_OK) return rc;
-  if ((rc = make_map(&prm.tm_v, v, tk, static_cast<int64_t>(hkv) * kD, v_row_stride)) != RCP_OK) return rc;
+  if ((rc = make_map(&prm.tm_q, q, tq, static_cast<int64_t>(hq) * kD, q_row_stride, kQRows)) != RCP_OK)
+    return rc;
+  if ((rc = make_map(&prm.tm_k, k, tk, static_cast<int64_t>(hkv) * kD, k_row_stride, kKRows)) != RCP_OK)
+    return rc;
+  if ((rc = make_map(&prm.tm_v, v, tk, static_cast<int64_t>(hkv) * kD, v_row_stride, kKRows)) != RCP_OK)
+    return rc;
   TileSum* qsum = static_cast<TileSum*>(workspace);
-  const int n_qtiles = static_cast<int>((tq + 127) / 128);
-  const int n_ktiles = static_cast<int>((tk + 127) / 128);
+  const int n_qtiles = static_cast<int>((tq + kQRows - 1) / kQRows);
+  const int n_kblocks = static_cast<int>((tk + kKRows - 1) / kKRows);
   TileSum* ksum = qsum + n_qtiles;
-  if ((rc = launch_tile_summary(q_pos, q_seq, tq, RCP_SEQ_PAD_Q, qsum, st)) != RCP_OK) return rc;
-  if ((rc = launch_tile_summary(k_pos, k_seq, tk, RCP_SEQ_PAD_K, ksum, st)) != RCP_OK) return rc;
+  if ((rc = launch_tile_summary(q_pos, q_seq, tq, RCP_SEQ_PAD_Q, kQRows, qsum, st)) != RCP_OK)
+    return rc;
+  if ((rc = launch_tile_summary(k_pos, k_seq, tk, RCP_SEQ_PAD_K, kKRows, ksum, st)) != RCP_OK)
+    return rc;
+  uint32_t* act = reinterpret_cast<uint32_t*>(ksum + n_kblocks);
+  const int n_qblk = (n_qtiles + 1) / 2;
+  int* act_n = reinterpret_cast<int*>(act + static_cast<int64_t>(n_qblk) * n_kblocks);
+  active_list_kernel<<<n_qblk, 256, 0, st>>>(qsum, ksum, n_qtiles, n_kblocks, act, act_n);
+  RCP_CUDA(cudaGetLastError());
+  prm.act = act;
+  prm.act_n = act_n;
   prm.q_pos = q_pos;
   prm.q_seq = q_seq;
   prm.k_pos = k_pos;
@@ -482,9 +678,10 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
   prm.group = hq / hkv;
   prm.n_qtiles = n_qtiles;
   prm.n_qblk = (n_qtiles + 1) / 2;
-  prm.n_ktiles = n_ktiles;
+  prm.n_kblocks = n_kblocks;
   prm.mode = mode;
   prm.scale_log2 = static_cast<float>(static_cast<double>(scale) * 1.4426950408889634);
+  prm.trace = g_trace;
 
   static bool attr_set = false;
   if (!attr_set) {

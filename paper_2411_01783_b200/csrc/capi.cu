@@ -21,11 +21,12 @@ void set_error(const char* fmt, ...) {
 }
 
 // ------------------------------------------------------------------ tile summary
+// One CTA of `rows` (64 or 128) threads per tile.
 __global__ void __launch_bounds__(128) tile_summary_kernel(const int32_t* __restrict__ pos,
                                                            const int32_t* __restrict__ seq,
                                                            int64_t n, int32_t pad_seq,
                                                            TileSum* __restrict__ out) {
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * 128 + threadIdx.x;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   int p = 0, s = 0;
   bool valid = false;
   if (row < n) {
@@ -55,24 +56,26 @@ __global__ void __launch_bounds__(128) tile_summary_kernel(const int32_t* __rest
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    TileSum t;
-    t.pmin = min(min(red[0][0], red[1][0]), min(red[2][0], red[3][0]));
-    t.pmax = max(max(red[0][1], red[1][1]), max(red[2][1], red[3][1]));
-    t.smin = min(min(red[0][2], red[1][2]), min(red[2][2], red[3][2]));
-    t.smax = max(max(red[0][3], red[1][3]), max(red[2][3], red[3][3]));
-    t.nvalid = red[0][4] + red[1][4] + red[2][4] + red[3][4];
-    t.uniform = (t.nvalid == 128 && t.smin == t.smax) ? 1 : 0;
+    TileSum t = {INT_MAX, INT_MIN, INT_MAX, INT_MIN, 0, 0, 0, 0};
+    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) {
+      t.pmin = min(t.pmin, red[i][0]);
+      t.pmax = max(t.pmax, red[i][1]);
+      t.smin = min(t.smin, red[i][2]);
+      t.smax = max(t.smax, red[i][3]);
+      t.nvalid += red[i][4];
+    }
+    t.uniform = (t.nvalid == static_cast<int>(blockDim.x) && t.smin == t.smax) ? 1 : 0;
     t.pad0 = t.pad1 = 0;
     out[blockIdx.x] = t;
   }
 }
 
 int launch_tile_summary(const int32_t* pos, const int32_t* seq, int64_t n, int32_t pad_seq,
-                        TileSum* out, cudaStream_t stream) {
-  const int64_t tiles = (n + 127) / 128;
+                        int rows, TileSum* out, cudaStream_t stream) {
+  const int64_t tiles = (n + rows - 1) / rows;
   if (tiles == 0) return RCP_OK;
-  tile_summary_kernel<<<static_cast<unsigned>(tiles), 128, 0, stream>>>(pos, seq, n, pad_seq,
-                                                                         out);
+  tile_summary_kernel<<<static_cast<unsigned>(tiles), rows, 0, stream>>>(pos, seq, n, pad_seq,
+                                                                          out);
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
 }

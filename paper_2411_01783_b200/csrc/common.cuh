@@ -62,8 +62,8 @@ __device__ __forceinline__ float merge_val(float a, float b, const MergeW& w) {
 }
 
 // ------------------------------------------------------------------ tile summaries
-// Per 128-token tile of a block: min/max position and sequence id over the
-// VALID rows, number of valid rows, and whether all 128 rows are valid and of
+// Per 64- or 128-token tile of a block: min/max position and sequence id over the
+// VALID rows, number of valid rows, and whether all rows are valid and of
 // one sequence.  Used to classify (query tile, key tile) pairs as empty / full
 // / partial so masked work is skipped and unmasked tiles skip the mask.
 struct __align__(32) TileSum {
@@ -80,8 +80,8 @@ __host__ __device__ __forceinline__ int classify_tile(const TileSum& q, const Ti
   return kTilePartial;
 }
 
-// Launch the summary kernel for one metadata array (n rows, 128-row tiles).
+// Launch the summary kernel for one metadata array (n rows, `rows`-row tiles, rows in {64, 128}).
 int launch_tile_summary(const int32_t* pos, const int32_t* seq, int64_t n, int32_t pad_seq,
-                        TileSum* out, cudaStream_t stream);
+                        int rows, TileSum* out, cudaStream_t stream);
 
 }  // namespace rcp

@@ -71,9 +71,28 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar_addr, uint32_t parity
 #ifndef RCP_WATCHDOG
 #define RCP_WATCHDOG 1
 #endif
+#ifdef RCP_TRACE_BUILD
+// Debug builds: the first timed-out wait records {block, thread, barrier smem
+// address, parity} here and the wait gives up instead of trapping.
+__device__ int g_hang_info[4];
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait(a, parity)) return;
+#ifdef RCP_TRACE_BUILD
+  const long long th0 = clock64();
+  while (!mbar_try_wait(a, parity)) {
+    if (clock64() - th0 > (1ll << 29)) {
+      if (atomicCAS(&g_hang_info[0], 0, 1 + static_cast<int>(blockIdx.x)) == 0) {
+        g_hang_info[1] = threadIdx.x;
+        g_hang_info[2] = static_cast<int>(a);
+        g_hang_info[3] = static_cast<int>(parity);
+      }
+      return;
+    }
+  }
+  return;
+#else
 #if RCP_WATCHDOG
   const long long t0 = clock64();
   while (!mbar_try_wait(a, parity)) {
@@ -82,6 +101,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #else
   while (!mbar_try_wait(a, parity)) {
   }
+#endif
 #endif
 }
 
@@ -198,6 +218,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
       : "r"(taddr)
       : "memory");
 }
+template <uint32_t kRegs>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+template <uint32_t kRegs>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
