@@ -12,7 +12,8 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_ringcp_b200.so")
+# RCP_LIB_PATH selects an alternative build of the same ABI (A/B experiments, trace builds).
+LIB_PATH = os.environ.get("RCP_LIB_PATH") or os.path.join(_PKG, "_ringcp_b200.so")
 
 RCP_OK = 0
 RCP_ERR_INVALID = -1

@@ -52,7 +52,10 @@ constexpr uint32_t kSmemBytes = 2 * kQTileBytes + kSlots * kKVBytes + 1024;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 // Of every 8 score pairs of a FULL block, this many take exp2 on the FMA pipe
 // (cubic polynomial) instead of MUFU.EX2, balancing the two pipes.
-constexpr int kPolyPairsPer8 = 2;
+#ifndef RCP_POLY_PAIRS
+#define RCP_POLY_PAIRS 2
+#endif
+constexpr int kPolyPairsPer8 = RCP_POLY_PAIRS;
 constexpr uint32_t kTmemO = 0, kTmemS = 256;  // column bases
 
 struct AttnParams {

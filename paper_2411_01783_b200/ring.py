@@ -265,14 +265,29 @@ def _cuda_merge(o_parts, l_parts, out, lse):
     merge_rows_into(o_parts, l_parts, out, lse)
 
 
+def _cuda_decode(q, k_arena, v_arena, starts, lens, max_len, cfg: GqaConfig, out, lse, ws=None):
+    """Split-KV decode of q [B, Hq, D] against arena rows [starts[b], starts[b]+lens[b])."""
+    lib = _lib.load()
+    B, H, D = q.shape
+    need = lib.rcp_decode_workspace_bytes(B, H, max(max_len, 1))
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 32), dtype=torch.uint8, device=q.device)
+    _lib.count("rcp_decode_attn")
+    _lib.check(lib.rcp_decode_attn(
+        _lib.ptr(q), _lib.ptr(k_arena), _lib.ptr(v_arena), k_arena.stride(0), _lib.ptr(starts),
+        _lib.ptr(lens), B, max(max_len, 1), H, cfg.n_kv_heads, D, float(cfg.scale), _lib.ptr(out),
+        _lib.ptr(lse), _lib.ptr(ws), ws.numel(), _lib.stream_handle()))
+
+
 class RingAttention:
     """SPMD ring attention for one rank.  ``attend``/``merge`` default to the
     sm_100a kernels; tests inject oracle callables to check the schedule on CPU."""
 
-    def __init__(self, comm, attend=None, merge=None, device=None):
+    def __init__(self, comm, attend=None, merge=None, decode=None, device=None):
         self.comm = comm
         self.attend = attend or _cuda_attend
         self.merge = merge or _cuda_merge
+        self.decode = decode or _cuda_decode
         self.device = device
         self._bufs = {}
         self.trace: StepTrace | None = None
@@ -423,9 +438,6 @@ class RingAttention:
         st_d = torch.from_numpy(starts).to(dev)
         ln_d = torch.from_numpy(lens).to(dev)
         max_len = int(lens.max()) if lens.size else 0
-        lib = _lib.load()
-        ws_bytes = lib.rcp_decode_workspace_bytes(slots, H, max(max_len, 1))
-        ws = self._buf(("dws",), max(ws_bytes, 32), dev)
         send_o = [torch.empty((slots, H, D), dtype=torch.float32, device=dev) for _ in range(n)]
         send_l = [torch.empty((slots, H), dtype=torch.float32, device=dev) for _ in range(n)]
         bufs = [self._buf(("dq", 0), qlay.nbytes, dev), self._buf(("dq", 1), qlay.nbytes, dev)]
@@ -440,12 +452,8 @@ class RingAttention:
                 if self.trace is not None:
                     self.trace.add(step, k, "Q", qlay.nbytes)
             q_cur, _, _ = qlay.views(cur)
-            _lib.count("rcp_decode_attn")
-            _lib.check(lib.rcp_decode_attn(
-                _lib.ptr(q_cur), _lib.ptr(cache.k), _lib.ptr(cache.v), cache.k.stride(0),
-                _lib.ptr(st_d[step]), _lib.ptr(ln_d[step]), slots, max(max_len, 1), H,
-                cfg.n_kv_heads, D, float(cfg.scale), _lib.ptr(send_o[src]), _lib.ptr(send_l[src]),
-                _lib.ptr(ws), ws.numel(), _lib.stream_handle()))
+            self.decode(q_cur, cache.k, cache.v, st_d[step], ln_d[step], max_len, cfg,
+                        send_o[src], send_l[src])
             self.comm.wait(works)
             cur = nxt
         recv_o = [torch.empty_like(send_o[0]) for _ in range(n)]
