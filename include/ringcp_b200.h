@@ -102,14 +102,15 @@ int rcp_fold_meta(const int64_t* pos, const int64_t* seq, const uint8_t* valid, 
 /* Split-KV decode attention: one query token per sequence against the rank's
  * cached KV shard of that sequence (ring pass-Q decode, Alg. 4,
  * PAPER.md:353-370).  q [B, hq, 128] bf16; for sequence b the keys are rows
- * [kv_start[b], kv_start[b] + kv_len[b]) of k/v ([rows, hkv, 128] bf16,
- * row stride kv_row_stride), all causally visible (cache holds only the
- * past and the token itself) and same-sequence.  kv_start/kv_len are device
- * int64 arrays.  Writes o [B, hq, 128] fp32, lse [B, hq] fp32 (-inf when
- * kv_len == 0).  workspace: rcp_decode_workspace_bytes(B, hq, max_len). */
+ * [kv_start[b], kv_start[b] + kv_len[b]) of the KV arena k/v ([kv_rows, hkv,
+ * 128] bf16, row stride kv_row_stride), all causally visible (the cache holds
+ * only the past and the token itself) and of the same sequence.  kv_start /
+ * kv_len are device int64 arrays; max_kv_len bounds kv_len.  hq / hkv <= 16.
+ * Writes o [B, hq, 128] fp32, lse [B, hq] fp32 (-inf when kv_len == 0).
+ * workspace: rcp_decode_workspace_bytes(B, hq, max_kv_len). */
 size_t rcp_decode_workspace_bytes(int64_t batch, int32_t hq, int64_t max_kv_len);
 int rcp_decode_attn(const void* q, const void* k, const void* v, int64_t kv_row_stride,
-                    const int64_t* kv_start, const int64_t* kv_len, int64_t batch,
+                    int64_t kv_rows, const int64_t* kv_start, const int64_t* kv_len, int64_t batch,
                     int64_t max_kv_len, int32_t hq, int32_t hkv, int32_t head_dim, float scale,
                     float* o, float* lse, void* workspace, size_t workspace_bytes, void* stream);
 

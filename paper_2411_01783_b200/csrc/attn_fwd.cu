@@ -205,9 +205,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   __shared__ uint32_t tmem_slot;
 
   const int warp = static_cast<int>(warp_id());
-  const int head = blockIdx.x % p.hq;
-  const int qblk = p.n_qblk - 1 - static_cast<int>(blockIdx.x / p.hq);  // late (heavy) blocks first
-  const int kvh = head / p.group;
+  // CTA order: KV-head major (consecutive CTAs share one KV head, so a wave of
+  // ~148 CTAs streams that head's K/V once from DRAM and later waves find it in
+  // the 126 MB L2), heavy (late) query blocks first inside a head, then the
+  // query heads of the GQA group.
+  const int per_kv = p.n_qblk * p.group;
+  const int kvh = static_cast<int>(blockIdx.x) / per_kv;
+  const int rem = static_cast<int>(blockIdx.x) - kvh * per_kv;
+  const int qblk = p.n_qblk - 1 - rem / p.group;
+  const int head = kvh * p.group + rem % p.group;
   if (threadIdx.x == 0) {
     mbar_init(&bar_q, 1);
     for (int s = 0; s < kSlots; ++s) {

@@ -99,6 +99,16 @@ class RankKvCache:
         self._used = 0
         self._segs.clear()
 
+    def truncate(self, seq_id: int, length: int) -> None:
+        """Drop every row of a sequence beyond the first `length` (restores the
+        cache to an earlier turn; rows are position-sorted, so this drops the
+        most recent tokens)."""
+        seg = self._segs.get(seq_id)
+        if seg is None or length >= seg.length:
+            return
+        seg.length = max(0, int(length))
+        seg.max_pos = int(self.pos[seg.start + seg.length - 1].item()) if seg.length else -1
+
     # ---------------------------------------------------------------- SPEC API
     def cached_len(self, seq_id: int) -> int:
         seg = self._segs.get(seq_id)

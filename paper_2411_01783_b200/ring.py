@@ -249,6 +249,28 @@ class TorchRingComm:
         recvs[self.rank].copy_(sends[self.rank])
         return works
 
+    def all_gather(self, inp: torch.Tensor, out: torch.Tensor):
+        """out = concat over ranks of inp (out.shape[0] = world * inp.shape[0])."""
+        m = inp.shape[0]
+        w = self.dist.all_gather([out[r * m:(r + 1) * m] for r in range(self.world)], inp,
+                                 group=self.group, async_op=True)
+        return [w]
+
+    def all_to_all_many(self, pairs):
+        """Several All2Alls in ONE grouped launch: pairs = [(sends, recvs), ...]."""
+        d = self.dist
+        ops = []
+        for sends, recvs in pairs:
+            for r in range(self.world):
+                if r == self.rank:
+                    continue
+                ops.append(d.P2POp(d.isend, sends[r], self._g(r), self.group))
+                ops.append(d.P2POp(d.irecv, recvs[r], self._g(r), self.group))
+        works = d.batch_isend_irecv(ops) if ops else []
+        for sends, recvs in pairs:
+            recvs[self.rank].copy_(sends[self.rank])
+        return works
+
     @staticmethod
     def wait(works):
         for w in works or []:
@@ -274,7 +296,8 @@ def _cuda_decode(q, k_arena, v_arena, starts, lens, max_len, cfg: GqaConfig, out
         ws = torch.empty(max(need, 32), dtype=torch.uint8, device=q.device)
     _lib.count("rcp_decode_attn")
     _lib.check(lib.rcp_decode_attn(
-        _lib.ptr(q), _lib.ptr(k_arena), _lib.ptr(v_arena), k_arena.stride(0), _lib.ptr(starts),
+        _lib.ptr(q), _lib.ptr(k_arena), _lib.ptr(v_arena), k_arena.stride(0), k_arena.shape[0],
+        _lib.ptr(starts),
         _lib.ptr(lens), B, max(max_len, 1), H, cfg.n_kv_heads, D, float(cfg.scale), _lib.ptr(out),
         _lib.ptr(lse), _lib.ptr(ws), ws.numel(), _lib.stream_handle()))
 
@@ -405,7 +428,8 @@ class RingAttention:
 
     # -------------------------------------------------------------- Alg. 4
     def pass_q_decode(self, plan: DecodePlan, cache: RankKvCache, q_tok: torch.Tensor,
-                      k_tok: torch.Tensor, v_tok: torch.Tensor, positions, cfg: GqaConfig):
+                      k_tok: torch.Tensor, v_tok: torch.Tensor, positions, cfg: GqaConfig,
+                      gather: bool = False):
         """Batched ring pass-Q decode for this rank.
 
         q_tok/k_tok/v_tok: [slots_per_rank, H, D] — this rank's assigned decode
@@ -414,12 +438,19 @@ class RingAttention:
         first (the query attends to itself), then queries rotate,
         every rank attends the visitors against its cached shard of their
         sequences, and an All2All returns the partials to the owner, merged in
-        pass-KV arrival order.  Returns (out [slots, Hq, D], lse [slots, Hq])."""
+        pass-KV arrival order.  Returns (out [slots, Hq, D], lse [slots, Hq]).
+
+        ``gather=True`` replaces the N-1 sequential (Q, bid) ring steps by ONE
+        all-gather of the (tiny) query blocks and ONE decode launch over every
+        visiting query: on an NVSwitch domain all ranks are equidistant, and the
+        partials and their merge order are those of the ring."""
         n, k = self.comm.world, self.comm.rank
         mine = plan.assignments[k]
         slots = plan.slots_per_rank
         for j, (sid, _b) in enumerate(mine):
             cache.append_rows(sid, k_tok[j:j + 1], v_tok[j:j + 1], [int(positions[j])])
+        if gather and n > 1:
+            return self._decode_gathered(plan, cache, q_tok, cfg)
         dev = cache.device
         H, D = cfg.n_query_heads, cfg.head_dim
         qlay = QLayout(slots, H, D)
@@ -466,6 +497,49 @@ class RingAttention:
         lse = torch.empty((slots, H), dtype=torch.float32, device=dev)
         order = [(k - j) % n for j in range(n)]
         self.merge([recv_o[s] for s in order], [recv_l[s] for s in order], out, lse)
+        return out, lse
+
+
+    def _decode_gathered(self, plan: DecodePlan, cache: RankKvCache, q_tok, cfg: GqaConfig):
+        n, k = self.comm.world, self.comm.rank
+        mine = plan.assignments[k]
+        slots = plan.slots_per_rank
+        dev = cache.device
+        H, D = cfg.n_query_heads, cfg.head_dim
+        q_mine = self._buf(("dg", "q"), slots * H * D * 2, dev).view(torch.bfloat16).view(slots, H, D)
+        q_mine.zero_()
+        if mine:
+            q_mine[: len(mine)].copy_(_bf16(q_tok[: len(mine)]))
+        q_all = self._buf(("dg", "qall"), n * slots * H * D * 2, dev).view(torch.bfloat16).view(n * slots, H, D)
+        wq = self.comm.all_gather(q_mine, q_all)
+        if self.trace is not None:
+            self.trace.add(0, k, "Q-allgather", q_mine.numel() * 2)
+        # kv segment of every (source rank, slot) query on this rank's cache
+        meta = np.zeros((2, n * slots), np.int64)
+        for src in range(n):
+            for j, (sid, _b) in enumerate(plan.assignments[src]):
+                meta[0, src * slots + j], meta[1, src * slots + j] = cache.segment(sid)
+        meta_t = torch.from_numpy(meta)
+        meta_d = meta_t.pin_memory().to(dev, non_blocking=True) if dev.type == "cuda" else meta_t
+        max_len = int(meta[1].max()) if meta.size else 0
+        part_o = torch.empty((n * slots, H, D), dtype=torch.float32, device=dev)
+        part_l = torch.empty((n * slots, H), dtype=torch.float32, device=dev)
+        self.comm.wait(wq)
+        self.decode(q_all, cache.k, cache.v, meta_d[0], meta_d[1], max_len, cfg, part_o, part_l)
+        recv_o = torch.empty_like(part_o)
+        recv_l = torch.empty_like(part_l)
+        so = [part_o[s * slots:(s + 1) * slots] for s in range(n)]
+        sl = [part_l[s * slots:(s + 1) * slots] for s in range(n)]
+        ro = [recv_o[s * slots:(s + 1) * slots] for s in range(n)]
+        rl = [recv_l[s * slots:(s + 1) * slots] for s in range(n)]
+        w = self.comm.all_to_all_many([(so, ro), (sl, rl)])
+        if self.trace is not None:
+            self.trace.add(0, k, "A2A", (n - 1) * slots * H * (D + 1) * 4)
+        self.comm.wait(w)
+        out = torch.empty((slots, H, D), dtype=torch.float32, device=dev)
+        lse = torch.empty((slots, H), dtype=torch.float32, device=dev)
+        order = [(k - j) % n for j in range(n)]
+        self.merge([ro[s] for s in order], [rl[s] for s in order], out, lse)
         return out, lse
 
 
@@ -577,6 +651,7 @@ def ring_pass_q_decode(plan: DecodePlan, caches: list, q_tok: torch.Tensor, k_to
             _lib.count("rcp_decode_attn")
             _lib.check(lib.rcp_decode_attn(
                 _lib.ptr(qb[b:b + 1]), _lib.ptr(caches[s].k), _lib.ptr(caches[s].v), caches[s].k.stride(0),
+                caches[s].k.shape[0],
                 _lib.ptr(st), _lib.ptr(ln), 1, max(length, 1), H, cfg.n_kv_heads, D, float(cfg.scale),
                 _lib.ptr(o), _lib.ptr(l), _lib.ptr(ws), ws.numel(), _lib.stream_handle()))
             parts_o.append(o)

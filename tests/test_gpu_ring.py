@@ -182,3 +182,34 @@ def _bf16(x):
     u = x.view(np.uint32).astype(np.uint64)
     r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
     return r.astype(np.uint32).view(np.float32)
+
+
+@pytest.mark.parametrize("hq,hkv,lens", [(128, 8, [5000, 70, 0, 1]), (32, 8, [4099, 64]),
+                                         (16, 1, [20000])])
+def test_decode_kernel_vs_oracle(rc, hq, hkv, lens):
+    """rcp_decode_attn directly: one query per sequence against its cache
+    segment (ragged lengths, empty segment, tail blocks, several splits)."""
+    import torch
+
+    from paper_2411_01783_b200.ring import _cuda_decode
+
+    rng = np.random.default_rng(sum(lens) + hq)
+    cap = sum(lens) + 256
+    k = _bf16(rng.standard_normal((cap, hkv, 128)))
+    v = _bf16(rng.standard_normal((cap, hkv, 128)))
+    q = _bf16(rng.standard_normal((len(lens), hq, 128)))
+    starts = np.cumsum([0] + lens[:-1]) + 3
+    cfg = rc.GqaConfig(hq, hkv, 128)
+    dev = lambda a: torch.from_numpy(a).cuda()
+    out = torch.empty((len(lens), hq, 128), dtype=torch.float32, device="cuda")
+    lse = torch.empty((len(lens), hq), dtype=torch.float32, device="cuda")
+    _cuda_decode(dev(q).to(torch.bfloat16), dev(k).to(torch.bfloat16), dev(v).to(torch.bfloat16),
+                 dev(starts.astype(np.int64)), dev(np.array(lens, np.int64)), max(lens), cfg, out, lse)
+    for b, n in enumerate(lens):
+        s0 = starts[b]
+        qb = orc.blk_from_tokens(q[b:b + 1], [n])
+        kb = orc.blk_from_tokens(k[s0:s0 + n], np.arange(n))
+        vb = orc.blk_from_tokens(v[s0:s0 + n], np.arange(n))
+        wo, wl = orc.gqa(qb, kb, vb, hkv)
+        assert np.abs(out[b].cpu().numpy() - wo[0]).max() <= G.O_TOL
+        assert G.lse_err(lse[b].cpu().numpy(), wl[0]) <= G.LSE_TOL

@@ -145,14 +145,15 @@ def _worker(rank, world, port, T, hq, hkv, errq):
             b_r = orc.materialize(seqs, world, r, [kd])
             v_r = orc.materialize(seqs, world, r, [vd])
             caches_o[r].append(5, b_r, v_r)
-        for it in range(2):
+        for it in range(4):
             dp = plan_decode(batch, world, it)
             tok_q = _bf16(rng.standard_normal((1, hq, D)))
             tok_k = _bf16(rng.standard_normal((1, hkv, D)))
             tok_v = _bf16(rng.standard_normal((1, hkv, D)))
             mine = dp.assignments[rank]
             o, l = ring.pass_q_decode(dp, cache, tok_q[: len(mine)] if mine else tok_q[:0],
-                                      tok_k[: len(mine)], tok_v[: len(mine)], [T + it] * len(mine), cfg)
+                                      tok_k[: len(mine)], tok_v[: len(mine)], [T + it] * len(mine), cfg,
+                                      gather=bool(it % 2))
             wo = orc.ring_decode(batch, world, it, caches_o, tok_q.float().numpy(), tok_k.float().numpy(),
                                  tok_v.float().numpy(), [T + it], hkv)
             if mine:

@@ -1,0 +1,193 @@
+"""Benchmarks for BASELINE configs #4 and #5 (launch with torchrun, one rank per GPU).
+
+  partial  cfg4: partial prefill on a persistent KV cache, P + T = 131072,
+           KV-cache miss rate sweep; times ring pass-KV and ring pass-Q for the
+           same turn and reports what the Alg. 1 heuristic (B200 profile) picks.
+  decode   cfg5: ring pass-Q batched decode, B sequences of `--context` cached
+           tokens sharded over the ranks (balanced prefill layout); times one
+           decode step (append + Q ring + split-KV attention + All2All + merge).
+
+Each measurement: warm-up, then per-step CUDA events on the compute stream,
+median over steps, max over ranks.  Prints one JSON line per point on rank 0.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2411_01783_b200 as rc  # noqa: E402
+from paper_2411_01783_b200 import perf_model as pm  # noqa: E402
+from paper_2411_01783_b200.kv_cache import RankKvCache  # noqa: E402
+from paper_2411_01783_b200.ring import RingAttention, TorchRingComm, _LocalComm  # noqa: E402
+from paper_2411_01783_b200.sharding import (SequenceSpec, materialize_rank_block, plan_decode,  # noqa: E402
+                                            plan_full_prefill, plan_partial_prefill)
+
+D = 128
+
+
+def setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def timed(fn, reset, steps, warmup, world):
+    for _ in range(warmup):
+        reset()
+        fn()
+    ts = []
+    for _ in range(steps):
+        reset()
+        barrier(world)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(max_over_ranks(s.elapsed_time(e), world))
+    return statistics.median(ts)
+
+
+def randn(shape, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return torch.randn(shape, generator=g, device="cuda", dtype=torch.bfloat16)
+
+
+def run_partial(args, rank, world):
+    hq, hkv = args.hq, args.hkv
+    cfg = rc.GqaConfig(hq, hkv, D)
+    total = args.context
+    comm = TorchRingComm() if world > 1 else _LocalComm(0, 1)
+    ring = RingAttention(comm)
+    m = pm.b200_profile(dict(n_query_heads=hq, n_kv_heads=hkv, head_dim=D), n_ranks=world)
+    quantum = 2 * world * 128
+    for miss in args.miss:
+        T = max(quantum, int(round(miss * total / quantum)) * quantum)
+        P = total - T
+        # history: a balanced prefill of P tokens placed the cache (rank r holds chunks r, 2N-1-r)
+        cache = RankKvCache(hkv, D, capacity_tokens=(P + T) // world + 8192)
+        layout = [[0] * world]
+        if P > 0:
+            hplan = plan_full_prefill([SequenceSpec(0, 0, P)], world)
+            kh = materialize_rank_block(hplan, rank, [randn((P, hkv, D), 21)])
+            vh = materialize_rank_block(hplan, rank, [randn((P, hkv, D), 22)])
+            loc = hplan.rank_local_indices(0, rank)
+            sl = np.nonzero(loc >= 0)[0]
+            cache.append_rows(0, kh.data[sl[0]:sl[-1] + 1], vh.data[sl[0]:sl[-1] + 1], loc[sl])
+            layout = [[hplan.new_token_count(0, r) for r in range(world)]]
+        plan = plan_partial_prefill([SequenceSpec(0, P, T)], world, layout)
+        qn, kn, vn = randn((T, hq, D), 31), randn((T, hkv, D), 32), randn((T, hkv, D), 33)
+        qb = materialize_rank_block(plan, rank, [qn])
+        kb = materialize_rank_block(plan, rank, [kn])
+        vb = materialize_rank_block(plan, rank, [vn])
+        base_len = cache.cached_len(0)
+        reset = lambda: cache.truncate(0, base_len)
+        res = {}
+        for proto in ("pass_kv", "pass_q"):
+            fn = (lambda: ring.pass_kv_prefill(plan, cache, qb, kb, vb, cfg)) if proto == "pass_kv" else \
+                 (lambda: ring.pass_q_prefill(plan, cache, qb, kb, vb, cfg))
+            res[proto] = timed(fn, reset, args.steps, args.warmup, world)
+        shape = pm.PrefillShape(T, P)
+        pick = pm.choose_strategy(shape, m)
+        pick_ref = pm.choose_strategy(shape, m, refined=True)
+        flops = 4.0 * D * hq * (T * P + T * (T + 1) / 2)
+        if rank == 0:
+            best = min(res, key=res.get)
+            print(json.dumps({
+                "config": "cfg4-partial-prefill", "cp": world, "n_q_heads": hq, "n_kv_heads": hkv,
+                "P": P, "T": T, "miss": T / total, "pass_kv_ms": res["pass_kv"], "pass_q_ms": res["pass_q"],
+                "winner": best, "heuristic": pick, "heuristic_refined": pick_ref,
+                "tflops_per_gpu_best": flops / (res[best] * 1e-3) / 1e12 / world}), flush=True)
+        del cache
+
+
+def run_decode(args, rank, world):
+    hq, hkv = args.hq, args.hkv
+    cfg = rc.GqaConfig(hq, hkv, D)
+    comm = TorchRingComm() if world > 1 else _LocalComm(0, 1)
+    ring = RingAttention(comm)
+    local = args.context // world
+    for B in args.batch:
+        cache = RankKvCache(hkv, D, capacity_tokens=B * (local + 64))
+        batch = list(range(B))
+        hplan = plan_full_prefill([SequenceSpec(0, 0, args.context)], world)
+        loc = hplan.rank_local_indices(0, rank)
+        pos = loc[loc >= 0]
+        for b in batch:  # each sequence: its balanced shard of the history (random data)
+            cache.append_rows(b, randn((local, hkv, D), 100 + b), randn((local, hkv, D), 200 + b), pos)
+        lens = {b: cache.cached_len(b) for b in batch}
+        dp = plan_decode(batch, world, 0)
+        mine = dp.assignments[rank]
+        n_mine = max(len(mine), 1)
+        qt, kt, vt = randn((n_mine, hq, D), 7), randn((n_mine, hkv, D), 8), randn((n_mine, hkv, D), 9)
+        positions = [args.context] * len(mine)
+
+        def reset():
+            for b in batch:
+                cache.truncate(b, lens[b])
+
+        def step():
+            return ring.pass_q_decode(dp, cache, qt[: len(mine)], kt[: len(mine)], vt[: len(mine)], positions, cfg,
+                                      gather=args.gather)
+
+        ms = timed(step, reset, args.steps, args.warmup, world)
+        kv_bytes = B * local * hkv * D * 2 * 2  # this rank's K+V read per decode step
+        if rank == 0:
+            print(json.dumps({
+                "config": "cfg5-ring-pass-q-decode", "cp": world, "batch": B, "context": args.context,
+                "q_transport": "allgather" if args.gather else "ring",
+                "n_q_heads": hq, "n_kv_heads": hkv, "step_ms": ms,
+                "kv_bytes_per_rank": kv_bytes, "hbm_gbs_effective": kv_bytes / (ms * 1e-3) / 1e9}), flush=True)
+        del cache
+        torch.cuda.empty_cache()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("mode", choices=["partial", "decode"])
+    ap.add_argument("--hq", type=int, default=128)
+    ap.add_argument("--hkv", type=int, default=8)
+    ap.add_argument("--context", type=int, default=131072)
+    ap.add_argument("--miss", type=float, nargs="*", default=[0.01, 0.025, 0.05, 0.10, 0.125, 0.2, 0.5, 1.0])
+    ap.add_argument("--batch", type=int, nargs="*", default=[1, 2, 4, 8, 16, 32])
+    ap.add_argument("--gather", action="store_true", help="decode: all-gather Q instead of the Q ring")
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=2)
+    args = ap.parse_args()
+    rank, world = setup()
+    try:
+        (run_partial if args.mode == "partial" else run_decode)(args, rank, world)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
