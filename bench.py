@@ -119,28 +119,40 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------- CPU arms
-def _oracle_sample(T, hq, hkv, rows, seed=7):
-    """Bounded sample of the same workload for the oracle port: `rows` query
-    rows spread over the sequence, attending to every key (causal)."""
+def _oracle_worker(args):
+    """Bounded sample of the workload for the oracle port: `rows` query rows
+    spread over the second half of the sequence, each attending (causally) to
+    all T keys, evaluated one query head at a time so the oracle's fp64
+    temporaries stay ~0.4 GB per worker.  Returns (seconds, admitted pairs)."""
+    T, hq, hkv, rows, seed = args
     from oracle import ringcp_oracle as orc
 
     rng = np.random.default_rng(seed)
     q_pos = np.linspace(T // 2, T - 1, rows).astype(np.int64)
-    q = orc.blk_from_tokens(rng.standard_normal((rows, hq, D)).astype(np.float32), q_pos)
-    k = orc.blk_from_tokens(rng.standard_normal((T, hkv, D)).astype(np.float32), np.arange(T))
-    v = orc.blk_from_tokens(rng.standard_normal((T, hkv, D)).astype(np.float32), np.arange(T))
-    pairs = int((q_pos + 1).sum())
-    return q, k, v, pairs
+    qd = rng.standard_normal((rows, hq, D)).astype(np.float32)
+    kd = rng.standard_normal((T, hkv, D)).astype(np.float32)
+    vd = rng.standard_normal((T, hkv, D)).astype(np.float32)
+    kpos = np.arange(T)
+    dt = 0.0
+    for h in range(hq):
+        g = (h * hkv) // hq  # GqaConfig.query_to_kv_head (attention.py:64-66)
+        q = orc.blk_from_tokens(qd[:, h:h + 1], q_pos)
+        k = orc.blk_from_tokens(kd[:, g:g + 1], kpos)
+        v = orc.blk_from_tokens(vd[:, g:g + 1], kpos)
+        t0 = time.perf_counter()
+        orc.gqa(q, k, v, 1, 1.0 / np.sqrt(D))
+        dt += time.perf_counter() - t0
+    return dt, int((q_pos + 1).sum())
 
 
-def _oracle_worker(args):
-    T, hq, hkv, rows, seed = args
-    from oracle import ringcp_oracle as orc
-
-    q, k, v, pairs = _oracle_sample(T, hq, hkv, rows, seed)
-    t0 = time.perf_counter()
-    orc.gqa(q, k, v, hkv)
-    return time.perf_counter() - t0, pairs
+def _worker_budget(cores: int) -> int:
+    """Parallel oracle workers: all cores, bounded by ~1.5 GB of host memory each."""
+    try:
+        with open("/proc/meminfo") as f:
+            avail = next(int(l.split()[1]) for l in f if l.startswith("MemAvailable")) / 1e6
+        return max(1, min(cores, int(avail // 1.5)))
+    except Exception:
+        return max(1, min(cores, 8))
 
 
 def cpu_baseline_port(T, hq, hkv, rows=16):
@@ -161,6 +173,7 @@ def run_reference(args, cfg, rank, world):
 
     T, hq, hkv = cfg["T"], cfg["hq"], cfg["hkv"]
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    cores = _worker_budget(cores)
     rows_per = 2
     jobs = [(T, hq, hkv, rows_per, 100 + i) for i in range(cores)]
     ctx = mp.get_context("fork")
@@ -285,6 +298,26 @@ def run_ours(args, cfg, rank, world, local_rank):
     achieved = per_launch_flops / (attn_avg_ms * 1e-3) / 1e12
     attn_share = sum(attn_ms) / (ms_rank * args.steps)
 
+    # ---------------- exposed communication: same kernels, transfers replaced by no-ops
+    exposed = None
+    if world > 1:
+        ring.no_comm = True
+        for _ in range(max(1, args.warmup - 1)):
+            step()
+        barrier()
+        c0 = torch.cuda.Event(enable_timing=True)
+        c1 = torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(args.steps):
+            step()
+        c1.record()
+        barrier()
+        ring.no_comm = False
+        ms_compute = max_over_ranks(c0.elapsed_time(c1) / args.steps)
+        exposed = {"ring_ms": ms, "compute_only_ms": ms_compute,
+                   "exposed_frac": max(0.0, (ms - ms_compute) / ms),
+                   "kv_message_bytes": int(ring._bufs[("kv", "local")].numel())}
+
     # ---------------- e2e through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -353,6 +386,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "attn_share_of_step": attn_share},
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "exposed_comm": exposed,
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
@@ -369,7 +403,7 @@ def main():
     ap.add_argument("--seq-len", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-rows", type=int, default=16)
+    ap.add_argument("--cpu-rows", type=int, default=8)
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.seq_len:

@@ -314,6 +314,10 @@ class RingAttention:
         self.device = device
         self._bufs = {}
         self.trace: StepTrace | None = None
+        # Measurement hook: True replaces every ring transfer by a local no-op
+        # (each step re-reads this rank's own block) — same kernels and shapes,
+        # used to compute the exposed-communication fraction.
+        self.no_comm = False
 
     def _buf(self, key, nbytes, device):
         b = self._bufs.get(key)
@@ -334,7 +338,9 @@ class RingAttention:
         for step in range(n):
             works = None
             nxt = None
-            if step < n - 1:
+            if step < n - 1 and self.no_comm:
+                nxt = cur
+            elif step < n - 1:
                 nxt = bufs[step % 2]
                 works = self.comm.exchange(cur, nxt)
                 if self.trace is not None:
