@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2411_01783_b200 import _lib  # noqa: E402
 
-_lib.LIB_PATH = os.path.join(ROOT, "paper_2411_01783_b200", "_ringcp_b200_trace.so")
+_lib.LIB_PATH = os.path.join(ROOT, "paper_2411_01783_b200", os.environ.get("RCP_TRACE_LIB", "_ringcp_b200_trace.so"))
 lib = _lib.load()
 lib.rcp_debug_set_trace.argtypes = [ctypes.c_void_p]
 
@@ -55,6 +55,40 @@ for cta in range(2):
     print(f"  cycles/iteration {per_it:.0f} (TC ideal 1024 per 64-key block); softmax0 {sm0:.0f}, softmax1 {sm1:.0f}; "
           f"PV0 issue -> next S0 ready {wait0:.0f}")
 
+VER = os.environ.get("RCP_ATTN_VERSION", "6")
+if VER == "6":
+    for cta in (0, 1):
+        d = t[cta, 8:56]
+        print(f"v6 CTA {cta}: cycles/block {np.mean(np.diff(d[:, 2])):.0f} (TC ideal 2048 per 128-key block, 2 tiles); "
+              f"softmax0 {np.mean(d[:, 3] - d[:, 2]):.0f}, softmax1 {np.mean(d[:, 5] - d[:, 4]):.0f}")
+        print(f"   softmax0 phases: ld {np.mean(d[:, 8] - d[:, 2]):.0f}, mask+max {np.mean(d[:, 9] - d[:, 8]):.0f}, "
+              f"exp+st {np.mean(d[:, 10] - d[:, 9]):.0f}, sum/rescale {np.mean(d[:, 11] - d[:, 10]):.0f}, "
+              f"st wait+arrive {np.mean(d[:, 3] - d[:, 11]):.0f}")
+        print(f"   P0(it) -> S0(it+1) ready {np.mean(d[1:, 2] - d[:-1, 3]):.0f}; P1(it) -> S1(it+1) ready "
+              f"{np.mean(d[1:, 4] - d[:-1, 5]):.0f}; P0 done -> PV0 issued {np.mean(d[:, 0] - d[:, 3]):.0f}; "
+              f"P1 done -> PV1 issued {np.mean(d[:, 1] - d[:, 5]):.0f}")
+        print(f"   MMA: top->V ready {np.mean(d[1:, 12] - d[:-1, 14]):.0f}, V->PV0 (wait P0) {np.mean(d[:, 0] - d[:, 12]):.0f}, "
+              f"PV0->PV1 (S0 + wait P1) {np.mean(d[:, 1] - d[:, 0]):.0f}, PV1->commits {np.mean(d[:, 13] - d[:, 1]):.0f}, "
+              f"S1 issue {np.mean(d[1:, 14] - d[1:, 13]):.0f}; loads lead {np.mean(d[:, 0] - d[:, 7]):.0f}")
+    sys.exit(0)
+if VER == "5":
+    for cta in (0, 1):
+        d = t[cta, 8:56]
+        rk = cta & 1
+        s_rdy, p_done = d[:, 2 + 2 * rk], d[:, 3 + 2 * rk]
+        print(f"v5 CTA {cta}: cycles/block {np.mean(np.diff(s_rdy)):.0f} (TC ideal 1024 per 128-key block); "
+              f"softmax {np.mean(p_done - s_rdy):.0f}; S ready -> next S ready waits {np.mean(s_rdy[1:] - p_done[:-1]):.0f}")
+        print(f"   softmax: S ready -> max exchanged {np.mean(d[:, 12 + rk] - s_rdy):.0f}; "
+              f"last h=0 warp P-arrive - warp4 P-done {np.mean(d[:, 14] - p_done):.0f}; "
+              f"last h=1 warp P-arrive - warp4 P-done {np.mean(d[:, 15] - p_done):.0f}")
+        if rk == 0:
+            print(f"   leader MMA: P->PV issue {np.mean(d[:, 0] - p_done):.0f}, PV issue {np.mean(d[:, 8] - d[:, 0]):.0f}, "
+                  f"commits+wait K {np.mean(d[:, 9] - d[:, 8]):.0f}, S issue {np.mean(d[:, 10] - d[:, 9]):.0f}, "
+                  f"loop top->P wait done {np.mean(d[1:, 0] - d[:-1, 1]):.0f}, loads lead {np.mean(d[:, 0] - d[:, 7]):.0f}; "
+                  f"own last P-arrive -> PV issue {np.mean(d[:, 0] - d[:, 15]):.0f}")
+            print(f"   S(it) issued (end of iter it-2) -> S(it) ready at softmax: {np.mean(d[2:, 2] - d[:-2, 10]):.0f}; "
+                  f"PV(it-1) issue -> S(it+1) issued: {np.mean(d[1:, 10] - d[:-1, 0]):.0f}")
+    sys.exit(0)
 d = t[0, 16:60]
 print("softmax0 phases (cycles): ld->s", np.mean(d[:, 8] - d[:, 2]), " max/m", np.mean(d[:, 9] - d[:, 8]),
       " exp loop", np.mean(d[:, 10] - d[:, 9]), " sum/rescale", np.mean(d[:, 11] - d[:, 10]),
