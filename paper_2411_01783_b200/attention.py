@@ -45,8 +45,8 @@ def _device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def _as_tensor(x, dtype=None) -> torch.Tensor:
-    dev = _device()
+def _as_tensor(x, dtype=None, device=None) -> torch.Tensor:
+    dev = device if device is not None else _device()
     if isinstance(x, torch.Tensor):
         t = x.to(device=dev, dtype=dtype) if dtype is not None else x.to(device=dev)
     else:
@@ -97,10 +97,13 @@ class EmbeddingBlock:
 
     def __init__(self, data, positions, valid, seq_ids, *, validate: bool = True,
                  n_valid: int | None = None, meta32=None):
-        data = _as_tensor(data)
-        positions = _as_tensor(positions, torch.int64)
-        valid = _as_tensor(valid, torch.bool)
-        seq_ids = _as_tensor(seq_ids, torch.int64)
+        # Blocks built internally from prepared tensors (validate=False) stay on
+        # their device; user-supplied data moves to the CUDA device.
+        dev = data.device if (not validate and isinstance(data, torch.Tensor)) else None
+        data = _as_tensor(data, device=dev)
+        positions = _as_tensor(positions, torch.int64, dev)
+        valid = _as_tensor(valid, torch.bool, dev)
+        seq_ids = _as_tensor(seq_ids, torch.int64, dev)
         if data.dim() != 3:
             raise ValueError(f"data must be [tokens, heads, head_dim], got shape {tuple(data.shape)}")
         n = data.shape[0]
@@ -257,7 +260,7 @@ class PartialAttention:
     lse: torch.Tensor
 
     def __post_init__(self):
-        lse = _as_tensor(self.lse, torch.float32)
+        lse = _as_tensor(self.lse, torch.float32, self.output.data.device)
         if tuple(lse.shape) != (self.output.n_tokens, self.output.n_heads):
             raise ValueError(f"lse shape {tuple(lse.shape)} does not match output "
                              f"[{self.output.n_tokens}, {self.output.n_heads}]")

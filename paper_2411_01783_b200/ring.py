@@ -561,6 +561,20 @@ class _LocalComm:
     def wait(works):
         assert not works
 
+    # A single-rank SPMD run (world 1) uses these through RingAttention: every
+    # collective over one rank is the identity.
+    def all_to_all(self, sends: list, recvs: list):
+        assert self.world == 1, "_LocalComm collectives are for world 1"
+        recvs[0].copy_(sends[0])
+
+    def all_to_all_many(self, pairs):
+        for sends, recvs in pairs:
+            self.all_to_all(sends, recvs)
+
+    def all_gather(self, inp: torch.Tensor, out: torch.Tensor):
+        assert self.world == 1, "_LocalComm collectives are for world 1"
+        out.copy_(inp.reshape(out.shape))
+
 
 def ring_pass_kv_prefill(plan: ShardPlan, caches: list, q_blocks: list, k_blocks: list,
                          v_blocks: list, cfg: GqaConfig, trace: StepTrace | None = None):
