@@ -114,3 +114,20 @@ def ptr_array(ptrs):
 
 def i64_array(vals):
     return (_i64 * len(vals))(*[int(v) for v in vals])
+
+
+def h2d(arr, device):
+    """Host array -> device tensor without a host/device sync: staged through
+    pinned memory (torch's caching host allocator keeps the staging block alive
+    until the copy has run) and copied with non_blocking=True.  A pageable
+    source would make the copy wait for all earlier work on the stream."""
+    import numpy as np
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    if device is None or torch.device(device).type != "cuda":
+        return t
+    staged = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    staged.copy_(t)
+    return staged.to(device, non_blocking=True)
+

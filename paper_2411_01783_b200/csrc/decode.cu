@@ -270,28 +270,66 @@ __global__ void __launch_bounds__(kDecThreads) decode_mma_kernel(const __grid_co
   }
 }
 
-// Fold the splits of each (sequence, query head) row in ascending order.
-__global__ void decode_combine_kernel(const float* __restrict__ part_o,
-                                      const float* __restrict__ part_lse, int64_t rows,
-                                      int n_split, float* __restrict__ o, float* __restrict__ lse) {
-  const int64_t row = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
+// Fold the splits of each (sequence, query head) row: one CTA per row, warp w
+// online-merges splits w, w+8, w+16, ... (independent loads, so a warp keeps
+// several 512-byte partials in flight instead of one dependent chain), then
+// warp 0 folds the 8 warp partials in warp order.  Deterministic; the same
+// kernel serves every decode transport, so they stay bit-identical.
+constexpr int kCombineWarps = 8;
+__global__ void __launch_bounds__(kCombineWarps * 32) decode_combine_kernel(
+    const float* __restrict__ part_o, const float* __restrict__ part_lse, int64_t rows, int n_split,
+    float* __restrict__ o, float* __restrict__ lse) {
+  __shared__ float4 s_acc[kCombineWarps][32];
+  __shared__ float s_m[kCombineWarps], s_l[kCombineWarps];
+  const int64_t row = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float4* po = reinterpret_cast<const float4*>(part_o + row * n_split * 128);
-  float4 acc = po[lane];
-  float la = part_lse[row * n_split];
-  for (int s = 1; s < n_split; ++s) {
-    const float lb = part_lse[row * n_split + s];
-    const float4 bv = po[s * 32 + lane];
-    const MergeW w = merge_weights(la, lb);
-    acc.x = merge_val(acc.x, bv.x, w);
-    acc.y = merge_val(acc.y, bv.y, w);
-    acc.z = merge_val(acc.z, bv.z, w);
-    acc.w = merge_val(acc.w, bv.w, w);
-    la = w.lse;
+  const float* pl = part_lse + row * n_split;
+  float m = -INFINITY, l = 0.f;  // running max / sum of exp(lse_s - m) (natural log)
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+  for (int sp = warp; sp < n_split; sp += kCombineWarps) {
+    const float ls = __ldg(pl + sp);
+    const float4 v = __ldg(po + static_cast<int64_t>(sp) * 32 + lane);
+    if (ls == -INFINITY) continue;  // empty split (uniform across the warp)
+    const float mn = fmaxf(m, ls);
+    const float a = __expf(m - mn), b = __expf(ls - mn);
+    acc.x = acc.x * a + v.x * b;
+    acc.y = acc.y * a + v.y * b;
+    acc.z = acc.z * a + v.z * b;
+    acc.w = acc.w * a + v.w * b;
+    l = l * a + b;
+    m = mn;
   }
-  reinterpret_cast<float4*>(o + row * 128)[lane] = acc;
-  if (lane == 0) lse[row] = la;
+  s_acc[warp][lane] = acc;
+  if (lane == 0) {
+    s_m[warp] = m;
+    s_l[warp] = l;
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  float mt = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < kCombineWarps; ++w) mt = fmaxf(mt, s_m[w]);
+  float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+  float lt = 0.f;
+  if (mt != -INFINITY) {
+#pragma unroll
+    for (int w = 0; w < kCombineWarps; ++w) {
+      if (s_m[w] == -INFINITY) continue;
+      const float f = __expf(s_m[w] - mt);
+      const float4 a = s_acc[w][lane];
+      r.x += a.x * f;
+      r.y += a.y * f;
+      r.z += a.z * f;
+      r.w += a.w * f;
+      lt += s_l[w] * f;
+    }
+  }
+  const bool has = lt > 0.f;
+  const float inv = has ? 1.0f / lt : 0.f;
+  reinterpret_cast<float4*>(o + row * 128)[lane] = make_float4(r.x * inv, r.y * inv, r.z * inv, r.w * inv);
+  if (lane == 0) lse[row] = has ? mt + logf(lt) : -INFINITY;
 }
 
 // Keys per CTA: about 8 waves of 148 CTAs, at least 8 blocks per CTA.
@@ -401,7 +439,7 @@ extern "C" int rcp_decode_attn(const void* q, const void* k, const void* v, int6
   decode_mma_kernel<<<grid, kDecThreads, kDecSmemBytes, st>>>(prm);
   RCP_CUDA(cudaGetLastError());
   const int64_t rows = batch * hq;
-  decode_combine_kernel<<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
+  decode_combine_kernel<<<static_cast<unsigned>(rows), kCombineWarps * 32, 0, st>>>(
       prm.part_o, prm.part_lse, rows, n_split, o, lse);
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;

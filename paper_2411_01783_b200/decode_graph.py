@@ -1,0 +1,174 @@
+"""CUDA-graph replay of the batched decode step (Alg. 4 with all-gathered Q).
+
+A decode step of a fixed batch is a fixed sequence of launches: append the
+owners' new K/V rows to the cache arena, (N > 1) all-gather the ranks' query
+slots, one split-KV decode launch over every visiting query against this
+rank's shard, (N > 1) All2All of the partials, merge in ring-arrival order.
+At small batch the step is bound by host launch overhead (~300 us of Python /
+ctypes / allocator work per step at B = 1 against ~250 us of GPU time,
+DESIGN.md), so ``GraphedDecode`` captures those launches once and replays
+them; per step the host only does the cache bookkeeping and ONE pinned
+host->device copy of the step's metadata (arena rows to append to,
+positions, per-query KV segments).
+
+Static shapes: the batch, its slot assignment pattern and the arena must not
+change while a graph is live.  ``GraphedDecode`` reserves room for
+``max_steps`` more tokens per sequence up front (so the arena never moves),
+fixes the decode kernel's split bound at the reserved capacity, routes empty
+slots (ranks with fewer tokens this iteration) to a scratch arena row, and
+re-captures if the cache was reallocated anyway.  Results equal the eager
+``RingAttention.pass_q_decode`` up to the split boundaries of the split-KV
+reduction (tests/test_gpu_decode_graph.py checks both against the oracle).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .attention import GqaConfig, merge_rows_into
+from .kv_cache import RankKvCache
+from .ring import _cuda_decode
+from .sharding import plan_decode
+
+__all__ = ["GraphedDecode"]
+
+_SCRATCH_SEQ = -7  # cache-internal sequence id of the scratch row (never a query's id)
+
+
+class GraphedDecode:
+    """Replayable decode step for ``batch`` on this rank.
+
+    ``step(q_tok, k_tok, v_tok, positions)`` takes this rank's tokens of the
+    current iteration in ``plan_decode(batch, N, it).assignments[rank]`` order
+    (as ``RingAttention.pass_q_decode``) and returns views of the static
+    (out [slots, Hq, D], lse [slots, Hq]) buffers, valid until the next step.
+    """
+
+    def __init__(self, comm, cache: RankKvCache, cfg: GqaConfig, batch, max_steps: int = 256,
+                 first_iteration: int = 0):
+        if cache.device.type != "cuda":
+            raise RuntimeError("GraphedDecode needs the cache on a CUDA device")
+        self.comm, self.cache, self.cfg = comm, cache, cfg
+        self.batch = [int(b) for b in batch]
+        self.n, self.rank = comm.world, comm.rank
+        self.it = int(first_iteration)
+        self.slots = math.ceil(len(self.batch) / self.n)
+        self.max_steps = int(max_steps)
+        self.steps_left = self.max_steps
+        dev = cache.device
+        H, Hkv, D = cfg.n_query_heads, cfg.n_kv_heads, cfg.head_dim
+        S, R = self.slots, self.n * self.slots
+        # room for every future token of this graph's lifetime (owner rotation
+        # gives each rank about max_steps / N of them per sequence), plus a
+        # scratch row that absorbs the appends of empty slots
+        per_seq = math.ceil(self.max_steps / self.n) + 1
+        for sid in self.batch:
+            cache._reserve(sid, per_seq)
+        cache._reserve(_SCRATCH_SEQ, 1)
+        self.scratch_row = cache.segment(_SCRATCH_SEQ)[0]
+        self.max_len = max(cache._segs[s].cap for s in self.batch)
+        # static buffers (graph inputs / outputs)
+        self.q_in = torch.zeros((S, H, D), dtype=torch.bfloat16, device=dev)
+        self.k_in = torch.zeros((S, Hkv, D), dtype=cache.dtype, device=dev)
+        self.v_in = torch.zeros_like(self.k_in)
+        self.meta = torch.zeros(S + 2 * R, dtype=torch.int64, device=dev)   # rows | starts | lens
+        self.meta32 = torch.zeros(2 * S, dtype=torch.int32, device=dev)     # pos | seq of appends
+        self.q_all = torch.zeros((R, H, D), dtype=torch.bfloat16, device=dev)
+        self.part_o = torch.empty((R, H, D), dtype=torch.float32, device=dev)
+        self.part_l = torch.empty((R, H), dtype=torch.float32, device=dev)
+        self.recv_o = torch.empty_like(self.part_o)
+        self.recv_l = torch.empty_like(self.part_l)
+        self.out = torch.empty((S, H, D), dtype=torch.float32, device=dev)
+        self.lse = torch.empty((S, H), dtype=torch.float32, device=dev)
+        lib = _lib.load()
+        self.ws = torch.empty(max(int(lib.rcp_decode_workspace_bytes(R, H, self.max_len)), 32),
+                              dtype=torch.uint8, device=dev)
+        self.graph = None
+        self._arena_ptr = None
+
+    # ------------------------------------------------------------------ launches
+    def _launches(self):
+        c, S = self.cache, self.slots
+        rows = self.meta[:S]
+        c.k.index_copy_(0, rows, self.k_in)
+        c.v.index_copy_(0, rows, self.v_in)
+        c.pos.index_copy_(0, rows, self.meta32[:S])
+        c.seq.index_copy_(0, rows, self.meta32[S:])
+        R = self.n * S
+        starts, lens = self.meta[S:S + R], self.meta[S + R:]
+        if self.n == 1:
+            _cuda_decode(self.q_in, c.k, c.v, starts, lens, self.max_len, self.cfg, self.out, self.lse, self.ws)
+            return
+        d = self.comm.dist
+        d.all_gather_into_tensor(self.q_all, self.q_in, group=self.comm.group)
+        _cuda_decode(self.q_all, c.k, c.v, starts, lens, self.max_len, self.cfg, self.part_o, self.part_l,
+                     self.ws)
+        d.all_to_all_single(self.recv_o, self.part_o, group=self.comm.group)
+        d.all_to_all_single(self.recv_l, self.part_l, group=self.comm.group)
+        order = [(self.rank - j) % self.n for j in range(self.n)]
+        merge_rows_into([self.recv_o[s * S:(s + 1) * S] for s in order],
+                        [self.recv_l[s * S:(s + 1) * S] for s in order], self.out, self.lse)
+
+    def _capture(self):
+        self._launches()  # warm-up: lazy inits, NCCL communicators, function attributes
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._launches()
+        self.graph = g
+        self._arena_ptr = (self.cache.k.data_ptr(), self.cache.v.data_ptr(), self.cache.pos.data_ptr(),
+                           self.cache.seq.data_ptr())
+
+    # ------------------------------------------------------------------ per step
+    def _host_meta(self, mine, positions):
+        """Cache bookkeeping for this rank's appends + the step's metadata arrays."""
+        c, S, n = self.cache, self.slots, self.n
+        rows = np.full(S, self.scratch_row, np.int64)
+        pos32 = np.full(S, _lib.POS_PAD_K, np.int64)
+        seq32 = np.full(S, _lib.SEQ_PAD_K, np.int64)
+        for j, (sid, _b) in enumerate(mine):
+            seg = c._segs[sid]
+            p = int(positions[j])
+            if seg.length >= seg.cap or p <= seg.max_pos:
+                raise RuntimeError("GraphedDecode: sequence outgrew its reservation or positions went "
+                                   "backwards; create a new GraphedDecode")
+            rows[j] = seg.start + seg.length
+            seg.length += 1
+            seg.max_pos = p
+            pos32[j], seq32[j] = p, sid
+        plan = plan_decode(self.batch, n, self.it)
+        starts = np.zeros(n * S, np.int64)
+        lens = np.zeros(n * S, np.int64)
+        for src in range(n):
+            for j, (sid, _b) in enumerate(plan.assignments[src]):
+                starts[src * S + j], lens[src * S + j] = c.segment(sid)
+        return np.concatenate([rows, starts, lens]), np.concatenate([pos32, seq32]).astype(np.int32)
+
+    def step(self, q_tok: torch.Tensor, k_tok: torch.Tensor, v_tok: torch.Tensor, positions):
+        if self.steps_left <= 0:
+            raise RuntimeError("GraphedDecode: max_steps reached; create a new GraphedDecode")
+        plan = plan_decode(self.batch, self.n, self.it)
+        mine = plan.assignments[self.rank]
+        m = len(mine)
+        if m:
+            self.q_in[:m].copy_(q_tok[:m])
+            self.k_in[:m].copy_(k_tok[:m])
+            self.v_in[:m].copy_(v_tok[:m])
+        meta, meta32 = self._host_meta(mine, positions)
+        self.meta.copy_(_lib.h2d(meta, self.cache.device), non_blocking=True)
+        self.meta32.copy_(_lib.h2d(meta32, self.cache.device), non_blocking=True)
+        ptrs = (self.cache.k.data_ptr(), self.cache.v.data_ptr(), self.cache.pos.data_ptr(),
+                self.cache.seq.data_ptr())
+        if self.graph is None or ptrs != self._arena_ptr:
+            # the warm-up launch in _capture executes this step (capture only
+            # records), so the step's appends and outputs happen exactly once
+            self._capture()
+        else:
+            self.graph.replay()
+        self.it += 1
+        self.steps_left -= 1
+        return self.out[:m], self.lse[:m]

@@ -144,19 +144,51 @@ class RankKvCache:
         belong to seq_id and are in the given position order."""
         return self._append_rows(seq_id, k_rows, v_rows, np.asarray(positions, np.int64))
 
+    def append_tokens(self, seq_ids, k_rows: torch.Tensor, v_rows: torch.Tensor, positions) -> None:
+        """Batched decode append: row j of k_rows/v_rows is one new token of
+        sequence seq_ids[j] at positions[j].  All host bookkeeping (segment
+        reservation) happens first, then one scatter per arena array, so a
+        decode step costs a handful of launches instead of several per token.
+        Repeated sequences or out-of-order positions take the per-token path."""
+        ids = [int(s) for s in seq_ids]
+        pos = np.asarray(positions, np.int64).reshape(-1)
+        n = len(ids)
+        if n == 0:
+            return
+        if pos.shape[0] != n or k_rows.shape[0] != n or v_rows.shape[0] != n:
+            raise ValueError("append_tokens needs one k/v row and position per sequence id")
+        in_order = len(set(ids)) == n and all(
+            p > (self._segs[s].max_pos if s in self._segs else -1) for s, p in zip(ids, pos))
+        if not in_order:
+            for j, sid in enumerate(ids):
+                self._append_rows(sid, k_rows[j:j + 1], v_rows[j:j + 1], pos[j:j + 1])
+            return
+        rows = np.empty(n, np.int64)
+        for j, sid in enumerate(ids):
+            seg = self._reserve(sid, 1)
+            rows[j] = seg.start + seg.length
+            seg.length += 1
+            seg.max_pos = int(pos[j])
+        rows_d = _lib.h2d(rows, self.device)
+        meta_d = _lib.h2d(np.stack([pos, np.asarray(ids, np.int64)]).astype(np.int32), self.device)
+        self.k.index_copy_(0, rows_d, k_rows.to(self.dtype))
+        self.v.index_copy_(0, rows_d, v_rows.to(self.dtype))
+        self.pos.index_copy_(0, rows_d, meta_d[0])
+        self.seq.index_copy_(0, rows_d, meta_d[1])
+
     def _append_rows(self, seq_id, k_rows, v_rows, pos_host: np.ndarray) -> int:
         n = int(pos_host.shape[0])
         if n == 0:
             return self.cached_len(seq_id)
         if np.any(np.diff(pos_host) <= 0):
             order = np.argsort(pos_host, kind="stable")
-            sel = torch.from_numpy(order).to(self.device)
+            sel = _lib.h2d(order, self.device)
             k_rows, v_rows, pos_host = k_rows[sel], v_rows[sel], pos_host[order]
         seg = self._reserve(seq_id, n)
         a = seg.start + seg.length
         self.k[a:a + n].copy_(k_rows.to(self.dtype))
         self.v[a:a + n].copy_(v_rows.to(self.dtype))
-        self.pos[a:a + n].copy_(torch.from_numpy(pos_host.astype(np.int32)))
+        self.pos[a:a + n].copy_(_lib.h2d(pos_host.astype(np.int32), self.device))
         self.seq[a:a + n].fill_(int(seq_id))
         seg.length += n
         if pos_host[0] <= seg.max_pos:

@@ -200,7 +200,7 @@ def append_new_tokens(plan: ShardPlan, rank: int, cache: RankKvCache, k_block: E
         loc = plan.rank_local_indices(i, rank)
         slots = np.nonzero(loc >= 0)[0]
         if slots.size:
-            rows = torch.from_numpy(slots + off).to(k_block.data.device)
+            rows = _lib.h2d(slots + off, k_block.data.device)
             if slots[-1] - slots[0] + 1 == slots.size:  # contiguous: plain slice
                 a, b = off + int(slots[0]), off + int(slots[-1]) + 1
                 kr, vr = k_block.data[a:b], v_block.data[a:b]
@@ -453,8 +453,9 @@ class RingAttention:
         n, k = self.comm.world, self.comm.rank
         mine = plan.assignments[k]
         slots = plan.slots_per_rank
-        for j, (sid, _b) in enumerate(mine):
-            cache.append_rows(sid, k_tok[j:j + 1], v_tok[j:j + 1], [int(positions[j])])
+        if mine:
+            cache.append_tokens([sid for sid, _b in mine], k_tok[: len(mine)], v_tok[: len(mine)],
+                                [int(p) for p in positions[: len(mine)]])
         if gather and n > 1:
             return self._decode_gathered(plan, cache, q_tok, cfg)
         dev = cache.device
@@ -472,8 +473,8 @@ class RingAttention:
             src = (k - step) % n
             for j, (sid, _b) in enumerate(plan.assignments[src]):
                 starts[step, j], lens[step, j] = cache.segment(sid)
-        st_d = torch.from_numpy(starts).to(dev)
-        ln_d = torch.from_numpy(lens).to(dev)
+        st_d = _lib.h2d(starts, dev)
+        ln_d = _lib.h2d(lens, dev)
         max_len = int(lens.max()) if lens.size else 0
         send_o = [torch.empty((slots, H, D), dtype=torch.float32, device=dev) for _ in range(n)]
         send_l = [torch.empty((slots, H), dtype=torch.float32, device=dev) for _ in range(n)]
@@ -525,8 +526,7 @@ class RingAttention:
         for src in range(n):
             for j, (sid, _b) in enumerate(plan.assignments[src]):
                 meta[0, src * slots + j], meta[1, src * slots + j] = cache.segment(sid)
-        meta_t = torch.from_numpy(meta)
-        meta_d = meta_t.pin_memory().to(dev, non_blocking=True) if dev.type == "cuda" else meta_t
+        meta_d = _lib.h2d(meta, dev)
         max_len = int(meta[1].max()) if meta.size else 0
         part_o = torch.empty((n * slots, H, D), dtype=torch.float32, device=dev)
         part_l = torch.empty((n * slots, H), dtype=torch.float32, device=dev)

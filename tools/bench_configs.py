@@ -141,6 +141,7 @@ def run_decode(args, rank, world):
         loc = hplan.rank_local_indices(0, rank)
         pos = loc[loc >= 0]
         for b in batch:  # each sequence: its balanced shard of the history (random data)
+            cache._reserve(b, local + 64)  # room for the decode steps: no segment moves later
             cache.append_rows(b, randn((local, hkv, D), 100 + b), randn((local, hkv, D), 200 + b), pos)
         lens = {b: cache.cached_len(b) for b in batch}
         dp = plan_decode(batch, world, 0)
@@ -157,12 +158,29 @@ def run_decode(args, rank, world):
             return ring.pass_q_decode(dp, cache, qt[: len(mine)], kt[: len(mine)], vt[: len(mine)], positions, cfg,
                                       gather=args.gather)
 
+        if args.graph:
+            # CUDA-graph replay of the step (decode_graph.GraphedDecode): one
+            # capture, then every timed step is a replay; the cache keeps
+            # growing by one token per sequence per step, as in serving.
+            from paper_2411_01783_b200.decode_graph import GraphedDecode
+
+            gd = GraphedDecode(comm, cache, cfg, batch, max_steps=args.warmup + args.steps + 2)
+            pos0 = {b: max(lens[b], args.context) for b in batch}
+
+            def step():  # noqa: F811 - graphed variant
+                it = gd.it
+                own = plan_decode(batch, world, it).assignments[rank]
+                p = [pos0[sid] + it for sid, _b in own]
+                return gd.step(qt[: len(own)], kt[: len(own)], vt[: len(own)], p)
+
+            reset = lambda: None  # noqa: E731 - appends are part of the measured step
         ms = timed(step, reset, args.steps, args.warmup, world)
         kv_bytes = B * local * hkv * D * 2 * 2  # this rank's K+V read per decode step
         if rank == 0:
             print(json.dumps({
                 "config": "cfg5-ring-pass-q-decode", "cp": world, "batch": B, "context": args.context,
-                "q_transport": "allgather" if args.gather else "ring",
+                "q_transport": "allgather" if (args.gather or args.graph) else "ring",
+                "cuda_graph": bool(args.graph),
                 "n_q_heads": hq, "n_kv_heads": hkv, "step_ms": ms,
                 "kv_bytes_per_rank": kv_bytes, "hbm_gbs_effective": kv_bytes / (ms * 1e-3) / 1e9}), flush=True)
         del cache
@@ -178,6 +196,7 @@ def main():
     ap.add_argument("--miss", type=float, nargs="*", default=[0.01, 0.025, 0.05, 0.10, 0.125, 0.2, 0.5, 1.0])
     ap.add_argument("--batch", type=int, nargs="*", default=[1, 2, 4, 8, 16, 32])
     ap.add_argument("--gather", action="store_true", help="decode: all-gather Q instead of the Q ring")
+    ap.add_argument("--graph", action="store_true", help="decode: replay the step from a CUDA graph")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     args = ap.parse_args()
