@@ -331,13 +331,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         d2h = out_host.numel() * 4 + lse_host.numel() * 4
 
         def e2e_step():
+            # public host-buffer API: the rank's K/V and query chunks go H2D on a
+            # copy stream, the attention runs per query range as they land, and
+            # each range's final O / LSE returns D2H while later ranges compute
             cache.reset()
-            qb = materialize_rank_block(plan, rank, [host["q"]])
-            kb = materialize_rank_block(plan, rank, [host["k"]])
-            vb = materialize_rank_block(plan, rank, [host["v"]])
-            part = ring.pass_kv_prefill(plan, cache, qb, kb, vb, gcfg)
-            out_host.copy_(part.output.data, non_blocking=True)
-            lse_host.copy_(part.lse, non_blocking=True)
+            ring.pass_kv_prefill_host(plan, cache, [host["q"]], [host["k"]], [host["v"]], gcfg, out_host, lse_host)
 
         e2e_step()
         barrier()

@@ -328,11 +328,18 @@ class RingAttention:
 
     # -------------------------------------------------------------- Alg. 2
     def pass_kv(self, q, q_pos, q_seq, kv_lay: KvLayout, kv_msg: torch.Tensor, cfg: GqaConfig,
-                out: torch.Tensor, lse: torch.Tensor, dtype=torch.bfloat16):
+                out: torch.Tensor, lse: torch.Tensor, dtype=torch.bfloat16, q_splits=None, q_ready=None,
+                on_final=None):
         """Ring pass-KV over prepared buffers: q [S, Hq, D], kv_msg the local
-        flat KV message.  Writes the merged (out, lse) for this rank's queries."""
+        flat KV message.  Writes the merged (out, lse) for this rank's queries.
+
+        ``q_splits`` [(a, b), ...] runs every ring step as one launch per query
+        slot range (streamed host inputs): the first step's launch of range i
+        waits for ``q_ready[i]`` (a CUDA event), and ``on_final(i)`` is called
+        right after range i's last-step launch, when its rows are final."""
         n, k = self.comm.world, self.comm.rank
         dev = kv_msg.device
+        splits = q_splits or [(0, q.shape[0])]
         bufs = [self._buf(("kv", 0), kv_lay.nbytes, dev), self._buf(("kv", 1), kv_lay.nbytes, dev)]
         cur = kv_msg
         for step in range(n):
@@ -346,11 +353,116 @@ class RingAttention:
                 if self.trace is not None:
                     self.trace.add(step, k, "KV", kv_lay.nbytes)
             kk, vv, kp, ks = kv_lay.views(cur, dtype)
-            self.attend(q, q_pos, q_seq, kk, vv, kp, ks, cfg, out, lse,
-                        _lib.MODE_OVERWRITE if step == 0 else _lib.MODE_MERGE)
+            mode = _lib.MODE_OVERWRITE if step == 0 else _lib.MODE_MERGE
+            for i, (a, b) in enumerate(splits):
+                if step == 0 and q_ready is not None:
+                    torch.cuda.current_stream().wait_event(q_ready[i])
+                self.attend(q[a:b], q_pos[a:b], q_seq[a:b], kk, vv, kp, ks, cfg, out[a:b], lse[a:b], mode)
+                if step == n - 1 and on_final is not None:
+                    on_final(i)
             self.comm.wait(works)
             cur = nxt
         return out, lse
+
+    def _side_stream(self, key):
+        s = self._bufs.get(("stream", key))
+        if s is None:
+            s = torch.cuda.Stream()
+            self._bufs[("stream", key)] = s
+        return s
+
+    def pass_kv_prefill_host(self, plan: ShardPlan, cache: RankKvCache, q_host, k_host, v_host,
+                             cfg: GqaConfig, out_host: torch.Tensor, lse_host: torch.Tensor,
+                             n_sub: int | None = None) -> None:
+        """Alg. 2 for host-resident inputs and outputs, with the PCIe copies
+        overlapped with the attention.
+
+        q_host/k_host/v_host: per-sequence HOST tensors of the new tokens (pinned
+        for asynchronous copies).  out_host [S, Hq, D] fp32 / lse_host [S, Hq]
+        (pinned) receive this rank's merged result for its S query slots (the
+        rows of ``materialize_rank_block``).  K/V go to the device first (the
+        cache append and the KV message need them), the query slots follow in
+        ``n_sub`` ranges on a copy stream, every ring step runs one attention
+        launch per range, and each range's final rows go back on a second copy
+        stream as soon as its last launch is queued.  Returns when everything
+        is queued; the caller's stream is ordered after the device->host copies.
+        ``n_sub`` defaults to one range per 8192 query slots (about a thousand
+        CTAs per launch), at most 16."""
+        from .sharding import _host_index_map, materialize_rank_block
+
+        k = self.comm.rank
+        dev = cache.device
+        cur = torch.cuda.current_stream(dev)
+        s_in, s_out = self._side_stream("h2d"), self._side_stream("d2h")
+        H, D = cfg.n_query_heads, cfg.head_dim
+        idx, posv, seqv = _host_index_map(plan, k)
+        S = idx.shape[0]
+        # device buffers come from the caller's stream; the copy streams wait
+        # for it first, so no block still in use elsewhere is overwritten
+        q = torch.empty((S, H, D), dtype=torch.bfloat16, device=dev)
+        out = torch.empty((S, H, D), dtype=torch.float32, device=dev)
+        lse = torch.empty((S, H), dtype=torch.float32, device=dev)
+        s_in.wait_stream(cur)
+        with torch.cuda.stream(s_in):
+            kb = materialize_rank_block(plan, k, list(k_host), dev)
+            vb = materialize_rank_block(plan, k, list(v_host), dev)
+            kv_ready = torch.cuda.Event()
+            kv_ready.record(s_in)
+            qp = _lib.h2d(posv.astype(np.int32), dev)
+            qs = _lib.h2d(seqv.astype(np.int32), dev)
+            srcs = [t.reshape(t.shape[0], -1) for t in q_host]
+            seq_off = np.cumsum([0] + [t.shape[0] for t in srcs])  # idx rows are concatenated
+            qf = q.view(S, -1)
+            if n_sub is None:
+                n_sub = min(16, max(1, S // 8192))
+            step = max(256, -(-S // max(n_sub, 1)) // 256 * 256)
+            splits = [(a, min(S, a + step)) for a in range(0, S, step)]
+            q_ready = []
+            for a, b in splits:
+                seg = idx[a:b]
+                # contiguous runs of valid source rows; padding slots zeroed
+                j = 0
+                while j < seg.size:
+                    if seg[j] < 0:
+                        e = j
+                        while e < seg.size and seg[e] < 0:
+                            e += 1
+                        qf[a + j:a + e].zero_()
+                    else:
+                        g = int(seg[j])
+                        si = int(np.searchsorted(seq_off, g, side="right")) - 1
+                        e = j + 1
+                        while e < seg.size and seg[e] == seg[e - 1] + 1 and seg[e] < seq_off[si + 1]:
+                            e += 1
+                        lo = g - int(seq_off[si])
+                        qf[a + j:a + e].copy_(srcs[si][lo:lo + e - j], non_blocking=True)
+                    j = e
+                ev = torch.cuda.Event()
+                ev.record(s_in)
+                q_ready.append(ev)
+        for t in (kb.data, vb.data, qp, qs):  # made on s_in, read on the caller's stream
+            t.record_stream(cur)
+        cur.wait_event(kv_ready)
+        append_new_tokens(plan, k, cache, kb, vb)
+        lay = KvLayout(kv_message_len(plan), cache.n_kv_heads, cache.head_dim)
+        msg = self._buf(("kv", "local"), lay.nbytes, dev)
+        build_kv_message(plan, cache, msg)
+        s_out.wait_stream(cur)
+
+        def on_final(i):
+            a, b = splits[i]
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            s_out.wait_event(ev)
+            with torch.cuda.stream(s_out):
+                out_host[a:b].copy_(out[a:b], non_blocking=True)
+                lse_host[a:b].copy_(lse[a:b], non_blocking=True)
+
+        self.pass_kv(q, qp, qs, lay, msg, cfg, out, lse, cache.dtype, q_splits=splits, q_ready=q_ready,
+                     on_final=on_final)
+        for t in (out, lse):
+            t.record_stream(s_out)
+        cur.wait_stream(s_out)
 
     def pass_kv_prefill(self, plan: ShardPlan, cache: RankKvCache, q_block: EmbeddingBlock,
                         k_block: EmbeddingBlock, v_block: EmbeddingBlock, cfg: GqaConfig) -> PartialAttention:

@@ -1,0 +1,51 @@
+"""pass_kv_prefill_host (host inputs/outputs, PCIe copies overlapped with the
+attention) must equal pass_kv_prefill on device inputs bit for bit: the query
+slot ranges are multiples of 256 rows, so every CTA sees the same query tile
+pair and the same key blocks."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n_sub", [1, 3, 8])
+@pytest.mark.parametrize("partial", [False, True])
+def test_host_stream_equals_device_path(n_sub, partial):
+    from paper_2411_01783_b200.attention import GqaConfig
+    from paper_2411_01783_b200.kv_cache import RankKvCache
+    from paper_2411_01783_b200.ring import RingAttention, _LocalComm
+    from paper_2411_01783_b200.sharding import (SequenceSpec, materialize_rank_block, plan_full_prefill,
+                                                plan_partial_prefill)
+
+    hq, hkv, D = 8, 2, 128
+    cfg = GqaConfig(hq, hkv, D)
+    g = torch.Generator().manual_seed(1)
+    lens = [1700, 900]
+    cached = [600, 0] if partial else [0, 0]
+    seqs = [SequenceSpec(3, cached[0], lens[0]), SequenceSpec(8, cached[1], lens[1])]
+    plan = plan_partial_prefill(seqs, 1, [[c] for c in cached]) if partial else plan_full_prefill(seqs, 1)
+    mk = lambda *s: torch.randn(*s, generator=g).to(torch.bfloat16).pin_memory()
+    qh = [mk(n, hq, D) for n in lens]
+    kh = [mk(n, hkv, D) for n in lens]
+    vh = [mk(n, hkv, D) for n in lens]
+    hist = (mk(cached[0], hkv, D), mk(cached[0], hkv, D)) if partial else None
+
+    def fresh_cache():
+        c = RankKvCache(hkv, D, capacity_tokens=256)
+        if partial:
+            c.append_rows(3, hist[0].cuda(), hist[1].cuda(), np.arange(cached[0]))
+        return c
+
+    ring = RingAttention(_LocalComm(0, 1))
+    ref = ring.pass_kv_prefill(plan, fresh_cache(), materialize_rank_block(plan, 0, [t.cuda() for t in qh]),
+                               materialize_rank_block(plan, 0, [t.cuda() for t in kh]),
+                               materialize_rank_block(plan, 0, [t.cuda() for t in vh]), cfg)
+    S = ref.output.n_tokens
+    out_h = torch.full((S, hq, D), float("nan")).pin_memory()
+    lse_h = torch.full((S, hq), float("nan")).pin_memory()
+    ring.pass_kv_prefill_host(plan, fresh_cache(), qh, kh, vh, cfg, out_h, lse_h, n_sub=n_sub)
+    torch.cuda.synchronize()
+    assert torch.equal(out_h, ref.output.data.cpu())
+    assert torch.equal(lse_h, ref.lse.cpu())
