@@ -971,6 +971,21 @@ __global__ void __launch_bounds__(kThreads6, 1) attn_fwd_v6_kernel(const __grid_
 // softmax warpgroups per CTA split the 128 score columns (64 each) and
 // exchange the row max through shared memory once per block.
 // ======================================================================
+// S/P buffers of v5: three 128-column TMEM buffers after O (O 128 + 3 x 128 =
+// 512 columns), so S(j+3) is issued after PV(j) and the softmax of block j+1
+// finds S(j+1) ready even when P(j) of the slowest of the 16 softmax warps
+// (two SMs) is late.
+// Softmax column groups of v5: each of kSmWG2 warpgroups per CTA owns
+// 128 / kSmWG2 score columns of every row (4 -> 4 softmax warps per SMSP to
+// hide MUFU / TMEM latency: measured slower, 1050 vs 1114 TF/s; 2 -> 384 threads, the default).
+#ifndef RCP_V5_GROUPS
+#define RCP_V5_GROUPS 2
+#endif
+constexpr int kSmWG2 = RCP_V5_GROUPS;
+constexpr int kCols2 = 128 / kSmWG2;
+constexpr int kThreads2 = 128 + 128 * kSmWG2;
+static_assert(kSmWG2 == 2 || kSmWG2 == 4, "v5 softmax groups must be 2 or 4");
+constexpr int kSBuf2 = 3;
 constexpr int kKRows2 = 128;
 constexpr int kSlots2 = 11;
 constexpr uint32_t kSlot2Bytes = 16384;  // K half: 64 keys x 128 dims; V half: 128 keys x 64 dims
@@ -1030,12 +1045,24 @@ __device__ __forceinline__ void commit2_mc(uint64_t* bar) {
       "h"(static_cast<uint16_t>(3))
       : "memory");
 }
+// Remote arrive on the leader CTA's barrier.  Default .release.cta semantics
+// (as CUTLASS's ClusterBarrier::arrive): the consumer of P is the leader's
+// tcgen05.mma, ordered by tcgen05.fence::before_thread_sync on this side and
+// fence::after_thread_sync after the wait.  A .release.cluster arrive stalled
+// the arriving warp ~1000 cycles per block (tools/trace_attn.py, v5).
+#ifndef RCP_ARRIVE_CLUSTER_RELEASE
+#define RCP_ARRIVE_CLUSTER_RELEASE 0
+#endif
 __device__ __forceinline__ void arrive_leader(uint64_t* bar) {
+#if RCP_ARRIVE_CLUSTER_RELEASE
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & 0xFEFFFFFFu)
                : "memory");
+#else
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & 0xFEFFFFFFu) : "memory");
+#endif
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     attn_fwd_2cta_kernel(const __grid_constant__ AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
@@ -1044,9 +1071,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint8_t* sKV = smem + kQTileBytes;   // kSlots2 half blocks (K half / V half alternate)
 
   __shared__ uint64_t bar_q, bar_full[kSlots2], bar_empty[kSlots2];
-  __shared__ uint64_t bar_s[2], bar_p[2], bar_pv, bar_o;
+  __shared__ uint64_t bar_s[kSBuf2], bar_p[kSBuf2], bar_pv, bar_o;
   __shared__ uint32_t tmem_slot;
-  __shared__ float xch[2][128];
+  __shared__ float xch[kSmWG2][128];
 
   const int warp = static_cast<int>(warp_id());
   const int rank = static_cast<int>(cluster_rank());
@@ -1065,9 +1092,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&bar_full[s], 1);
       mbar_init(&bar_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kSBuf2; ++b) {
       mbar_init(&bar_s[b], 1);
-      mbar_init(&bar_p[b], 16);  // 8 softmax warps x 2 CTAs
+      mbar_init(&bar_p[b], 2 * 4 * kSmWG2);  // every softmax warp of both CTAs
     }
     mbar_init(&bar_pv, 1);
     mbar_init(&bar_o, 1);
@@ -1120,12 +1147,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (leader CTA)
-    // The whole warp runs the loop and computes the (warp-uniform) descriptors,
-    // so ptxas keeps them in uniform registers; one elected lane issues the
-    // tcgen05.mma / commit instructions (always the same lane: elect.sync picks
-    // the lowest active lane, and commits track that lane's MMAs).
-    if (rank == 0 && n > 0) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA, one elected lane)
+    if (rank == 0 && n > 0 && elect_one()) {
       const uint32_t idesc_s = make_idesc_bf16_f32(256, kKRows2, 0, 0);
       const uint32_t idesc_o = make_idesc_bf16_f32(256, kD, 0, 1);
       const uint32_t q_lo = sw128_desc_lo(smem_u32(sQ), 16);
@@ -1135,88 +1158,101 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         mbar_wait(&bar_full[ld % kSlots2], (ld / kSlots2) & 1);
         tc_fence_after();
       };
-      auto commit = [&](uint64_t* bar) {
-        if (elect_one()) commit2_mc(bar);
-        __syncwarp();
-      };
       auto issue_s = [&](int buf, uint32_t ld) {
         const uint32_t ka = k_lo + (((ld % kSlots2) * kSlot2Bytes) >> 4);
-        if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < kD / 16; ++kk)
-            mma2_ss_lo(tmem + kTmemS2 + buf * 128, q_lo + (((kk >> 2) * kQBoxBytes + (kk & 3) * 32) >> 4),
-                       ka + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
-        }
-        __syncwarp();
+        for (int kk = 0; kk < kD / 16; ++kk)
+          mma2_ss_lo(tmem + kTmemS2 + buf * 128, q_lo + (((kk >> 2) * kQBoxBytes + (kk & 3) * 32) >> 4),
+                     ka + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
       };
       auto issue_pv = [&](int buf, uint32_t ld, bool acc) {
         const uint32_t va = v_lo + (((ld % kSlots2) * kSlot2Bytes) >> 4);
-        if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < kKRows2 / 16; ++kk)
-            mma2_ts_lo(tmem + kTmemO2, tmem + kTmemS2 + buf * 128 + kk * 8, va + ((kk * 2048) >> 4), idesc_o,
-                       (acc || kk > 0) ? 1u : 0u);
-        }
-        __syncwarp();
+        for (int kk = 0; kk < kKRows2 / 16; ++kk)
+          mma2_ts_lo(tmem + kTmemO2, tmem + kTmemS2 + buf * 128 + kk * 8, va + ((kk * 2048) >> 4), idesc_o,
+                     (acc || kk > 0) ? 1u : 0u);
       };
       mbar_wait(&bar_q, 0);
-      wait_load(0);
-      issue_s(0, 0);
-      commit(&bar_s[0]);
-      commit(&bar_empty[0]);
-      if (n > 1) {
-        wait_load(2);
-        issue_s(1, 2);
-        commit(&bar_s[1]);
-        commit(&bar_empty[2 % kSlots2]);
+      for (int b = 0; b < kSBuf2 && b < n; ++b) {
+        wait_load(2 * b);
+        issue_s(b, 2 * b);
+        commit2_mc(&bar_s[b]);
+        commit2_mc(&bar_empty[(2 * b) % kSlots2]);
       }
+      int buf = 0;
+      uint32_t ph = 0;
       for (int it = 0; it < n; ++it) {
-        const int buf = it & 1;
         const bool last = it + 1 == n;
-        const uint32_t ldv = 2 * it + 1, ldk2 = 2 * it + 4;
+        const uint32_t ldv = 2 * it + 1, ldk2 = 2 * (it + kSBuf2);
         wait_load(ldv);
-        mbar_wait(&bar_p[buf], (it >> 1) & 1);
+        mbar_wait(&bar_p[buf], ph);
         tc_fence_after();
-        if (lane_id() == 0) TRACE(0, it);
+        TRACE(0, it);
         issue_pv(buf, ldv, it > 0);
-        if (lane_id() == 0) TRACE(8, it);
-        commit(last ? &bar_o : &bar_pv);
-        commit(&bar_empty[ldv % kSlots2]);
-        if (it + 2 < n) {
+        TRACE(8, it);
+        commit2_mc(last ? &bar_o : &bar_pv);
+        commit2_mc(&bar_empty[ldv % kSlots2]);
+        if (it + kSBuf2 < n) {
           wait_load(ldk2);
-          if (lane_id() == 0) TRACE(9, it);
+          TRACE(9, it);
           issue_s(buf, ldk2);
-          if (lane_id() == 0) TRACE(10, it);
-          commit(&bar_s[buf]);
-          commit(&bar_empty[ldk2 % kSlots2]);
+          TRACE(10, it);
+          commit2_mc(&bar_s[buf]);
+          commit2_mc(&bar_empty[ldk2 % kSlots2]);
         }
-        if (lane_id() == 0) TRACE(1, it);
+        TRACE(1, it);
+        if (++buf == kSBuf2) {
+          buf = 0;
+          ph ^= 1u;
+        }
       }
     }
+    __syncwarp();
+#if RCP_TRACE && !defined(RCP_TRACE_PERWARP)
+  } else if (warp == 3) {
+    // trace builds: an idle warp timestamps S and PV completions (MMA latency)
+    if (elect_one() && p.trace && n > 0) {
+      // completion order: S(0..kSBuf2-1), then PV(j), S(j+kSBuf2), PV(j+1), ...
+      for (int it = 0; it < kSBuf2 && it < n; ++it) {
+        mbar_wait(&bar_s[it], 0);
+        TRACE(11, it);
+      }
+      for (int it = 0; it + 1 < n; ++it) {
+        mbar_wait(&bar_pv, it & 1);
+        TRACE(14, it);
+        if (it + kSBuf2 < n) {
+          mbar_wait(&bar_s[it % kSBuf2], ((it + kSBuf2) / kSBuf2) & 1);
+          TRACE(11, it + kSBuf2);
+        }
+      }
+    }
+    __syncwarp();
+#endif
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax + epilogue (both CTAs)
-    const int h = (warp - 4) >> 2;                                // column half of the 128-key block
+    const int h = (warp - 4) >> 2;                                // column group of the 128-key block
     const int t = static_cast<int>(threadIdx.x) - 128 - 128 * h;  // row inside this CTA's tile
     const int row = (2 * qblk + rank) * kQRows + t;
     const bool row_ok = row < p.tq;
     const int my_pos = row_ok ? __ldg(p.q_pos + row) : -1;
     const int my_seq = row_ok ? __ldg(p.q_seq + row) : RCP_SEQ_PAD_Q;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
-    const uint32_t o_addr = lane_base + kTmemO2 + h * 64;
+    const uint32_t o_addr = lane_base + kTmemO2 + h * kCols2;
     const float sl2 = p.scale_log2;
     const uint64_t sl2x2 = f2(sl2, sl2);
-    float m = -INFINITY, l = 0.f;  // l: this half's partial row sum
+    float m = -INFINITY, l = 0.f;  // l: this group's partial row sum
+    const uint32_t row_bar = 1 + (warp & 3), row_bar_threads = 32 * kSmWG2;  // warps of this row quarter
     uint32_t e_next = n > 0 ? __ldg(act) : 0u;
     int it = 0;
     for (; it < n; ++it) {
-      const int buf = it & 1;
-      const uint32_t s_addr = lane_base + kTmemS2 + buf * 128 + h * 64;
-      const uint32_t p_addr = lane_base + kTmemS2 + buf * 128 + h * 32;
+      const int buf = it % kSBuf2;
+      const uint32_t s_addr = lane_base + kTmemS2 + buf * 128 + h * kCols2;
+      const uint32_t p_addr = lane_base + kTmemS2 + buf * 128 + h * (kCols2 / 2);
       const uint32_t e = e_next;
       if (it + 1 < n) e_next = __ldg(act + it + 1);
       const int j = act_j(e);
       const int cls = act_cls(e, rank);
-      mbar_wait(&bar_s[buf], (it >> 1) & 1);
+      mbar_wait(&bar_s[buf], (it / kSBuf2) & 1);
       tc_fence_after();
       if (t == 0 && h == 0) TRACE(2 + 2 * rank, it);
 #if RCP_TRACE
@@ -1224,20 +1260,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         (void)0;
 #endif
       if (cls != kTileEmpty) {  // uniform across the CTA
-        uint32_t sr[64];
-        tmem_ld32(s_addr, sr);
-        tmem_ld32(s_addr + 32, sr + 32);
-        tmem_ld_wait();
-        float s[64];
+        uint32_t sr[kCols2];
 #pragma unroll
-        for (int c = 0; c < 64; ++c) s[c] = __uint_as_float(sr[c]);
+        for (int c = 0; c < kCols2; c += 32) tmem_ld32(s_addr + c, sr + c);
+        tmem_ld_wait();
+        float s[kCols2];
+#pragma unroll
+        for (int c = 0; c < kCols2; ++c) s[c] = __uint_as_float(sr[c]);
         if (cls == kTilePartial) {
-          const int base = j * kKRows2 + h * 64;
+          const int base = j * kKRows2 + h * kCols2;
           if (j * kKRows2 + kKRows2 <= p.tk) {
             const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + base);
             const int4* ks4 = reinterpret_cast<const int4*>(p.k_seq + base);
 #pragma unroll
-            for (int c4 = 0; c4 < 16; ++c4) {
+            for (int c4 = 0; c4 < kCols2 / 4; ++c4) {
               const int4 kp = __ldg(kp4 + c4), kq = __ldg(ks4 + c4);
               if (!(kq.x == my_seq && kp.x <= my_pos)) s[4 * c4 + 0] = -INFINITY;
               if (!(kq.y == my_seq && kp.y <= my_pos)) s[4 * c4 + 1] = -INFINITY;
@@ -1246,7 +1282,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           } else {
 #pragma unroll
-            for (int c = 0; c < 64; ++c) {
+            for (int c = 0; c < kCols2; ++c) {
               const int kidx = base + c;
               const bool ok = kidx < p.tk && __ldg(p.k_seq + kidx) == my_seq &&
                               __ldg(p.k_pos + kidx) <= my_pos;
@@ -1258,16 +1294,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < 8; ++k) m8[k] = s[k];
 #pragma unroll
-        for (int c = 8; c < 64; c += 8)
+        for (int c = 8; c < kCols2; c += 8)
 #pragma unroll
           for (int k = 0; k < 8; ++k) m8[k] = fmaxf(m8[k], s[c + k]);
         float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                          fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-        // Both halves have read their S columns before either writes P (P of
-        // the block reuses the first 64 columns of the S buffer).
+        // Row max over the groups (same order everywhere -> identical m).  All
+        // groups have read their S columns once this barrier passes, so P
+        // (the first 64 columns of the buffer) may overwrite S from here on.
         xch[h][t] = mx;
-        named_bar_sync(1, 256);
-        mx = fmaxf(mx, xch[h ^ 1][t]);
+        named_bar_sync(row_bar, row_bar_threads);
+        mx = xch[0][t];
+#pragma unroll
+        for (int g = 1; g < kSmWG2; ++g) mx = fmaxf(mx, xch[g][t]);
         if (t == 0 && h == 0) TRACE(12 + rank, it);
         const float m_old = m;
         const float m_new = fmaxf(m, mx * sl2);
@@ -1276,10 +1315,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const float m_use = (m == -INFINITY) ? 0.f : m;
         const uint64_t negm2 = f2(-m_use, -m_use);
         uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
-        uint32_t pk[32];
+        uint32_t pk[kCols2 / 2];
         if (cls == kTileFull) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
+          for (int i = 0; i < kCols2 / 2; ++i) {
             const float2 x = unf2(ffma2(f2(s[2 * i], s[2 * i + 1]), sl2x2, negm2));
             float p0, p1;
             if ((i & 7) < kPolyPairsPer8) {
@@ -1294,14 +1333,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
+          for (int i = 0; i < kCols2 / 2; ++i) {
             const float2 x = unf2(ffma2(f2(s[2 * i], s[2 * i + 1]), sl2x2, negm2));
             const float p0 = ex2_approx(x.x), p1 = ex2_approx(x.y);
             acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
             pk[i] = pack_bf16x2(p0, p1);
           }
         }
-        tmem_st32(p_addr, pk);
+        if (kCols2 == 64) tmem_st32(p_addr, pk);
+        else tmem_st16(p_addr, pk);
         const float2 a01 = unf2(fadd2(acc2[0], acc2[1]));
         const float2 a23 = unf2(fadd2(acc2[2], acc2[3]));
         const float sum = (a01.x + a01.y) + (a23.x + a23.y);
@@ -1311,7 +1351,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(&bar_pv, (it - 1) & 1);
           tc_fence_after();
 #pragma unroll
-          for (int c = 0; c < 64; c += 32) {
+          for (int c = 0; c < kCols2; c += 32) {
             uint32_t r[32];
             tmem_ld32(o_addr + c, r);
             tmem_ld_wait();
@@ -1321,20 +1361,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       } else {
-        uint32_t pk[32];
+        uint32_t pk[kCols2 / 2];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) pk[i] = 0u;
-        tmem_st32(p_addr, pk);
+        for (int i = 0; i < kCols2 / 2; ++i) pk[i] = 0u;
+        if (kCols2 == 64) tmem_st32(p_addr, pk);
+        else tmem_st16(p_addr, pk);
       }
       tmem_st_wait();
       tc_fence_before();
       if (t == 0 && h == 0) TRACE(3 + 2 * rank, it);
       __syncwarp();
       if ((threadIdx.x & 31) == 0) arrive_leader(&bar_p[buf]);
-#if RCP_TRACE
+      if (t == 0 && h == 0 && rank == 0) TRACE(15, it);
+#if RCP_TRACE && defined(RCP_TRACE_PERWARP)
       if ((threadIdx.x & 31) == 0 && p.trace && blockIdx.x < kTraceCtas && it < kTraceIters)
-        atomicMax(reinterpret_cast<unsigned long long*>(p.trace) + (blockIdx.x * kTraceIters + it) * kTraceEv + 14 + h,
-                  static_cast<unsigned long long>(clock64()));
+        p.trace[(blockIdx.x * kTraceIters + it) * kTraceEv + 8 + (warp - 4)] = clock64();
 #endif
     }
     // epilogue: combine the halves' sums, O / l, LSE, optional merge
@@ -1345,12 +1386,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const bool merge = p.mode == RCP_MODE_MERGE;
     if (!(merge && it == 0)) {
       xch[h][t] = l;
-      named_bar_sync(1, 256);
-      l += xch[h ^ 1][t];
+      named_bar_sync(row_bar, row_bar_threads);
+      l = xch[0][t];
+#pragma unroll
+      for (int g = 1; g < kSmWG2; ++g) l += xch[g][t];
       const bool has = l > 0.f;
       const float inv = has ? 1.0f / l : 0.f;
       const float lse_new = has ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
-      float* orow = p.o + (static_cast<int64_t>(row) * p.hq + head) * kD + h * 64;
+      float* orow = p.o + (static_cast<int64_t>(row) * p.hq + head) * kD + h * kCols2;
       float* lrow = p.lse + static_cast<int64_t>(row) * p.hq + head;
       MergeW mw;
       mw.lse = lse_new;
@@ -1358,7 +1401,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mw.wb = 1.f;
       if (merge && row_ok) mw = merge_weights(__ldg(lrow), lse_new);
 #pragma unroll
-      for (int c = 0; c < 64; c += 32) {
+      for (int c = 0; c < kCols2; c += 32) {
         uint32_t r[32];
         if (it > 0) {
           tmem_ld32(o_addr + c, r);
@@ -1382,7 +1425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (merge) named_bar_sync(1, 256);  // both halves read the old LSE before it is overwritten
+      if (merge) named_bar_sync(row_bar, row_bar_threads);  // every group read the old LSE before it is overwritten
       if (row_ok && h == 0) *lrow = merge ? mw.lse : lse_new;
     }
   }
@@ -1554,7 +1597,7 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
                                     kSmem2Bytes));
       attr2 = true;
     }
-    attn_fwd_2cta_kernel<<<static_cast<unsigned>(2 * grid), kThreads, kSmem2Bytes, st>>>(prm);
+    attn_fwd_2cta_kernel<<<static_cast<unsigned>(2 * grid), kThreads2, kSmem2Bytes, st>>>(prm);
   } else if (version == 6) {
     static bool attr6 = false;
     if (!attr6) {

@@ -60,15 +60,27 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 constexpr uint32_t kMbarSuspendHintNs = RCP_MBAR_HINT_NS;
 __device__ __forceinline__ bool mbar_try_wait(uint32_t bar_addr, uint32_t parity) {
   uint32_t ok;
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
-      "selp.u32 %0, 1, 0, p;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(bar_addr), "r"(parity), "n"(kMbarSuspendHintNs)
-      : "memory");
+  if (kMbarSuspendHintNs != 0) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(bar_addr), "r"(parity), "n"(kMbarSuspendHintNs)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(bar_addr), "r"(parity)
+        : "memory");
+  }
   return ok != 0;
 }
 // Spin on an mbarrier phase.  With RCP_WATCHDOG (default on) a wait that

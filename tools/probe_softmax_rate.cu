@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(256, 1) sm_probe(const float* in, float sl2, u
   }
   const long long t1 = clock64();
   sink[blockIdx.x * blockDim.x + threadIdx.x] = x_or ^ __float_as_uint(l);
-  if (threadIdx.x == 0) out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  if ((threadIdx.x & 31) == 0) out[blockIdx.x * 8 + (threadIdx.x >> 5)] = (unsigned long long)(t1 - t0);
 }
 
 // Instruction-form variants of the same loop (poly = 2 of 8 pairs, scalar cubic):
@@ -153,18 +153,20 @@ __global__ void __launch_bounds__(256, 1) form_probe(const float* in, float sl2,
   }
   const long long t1 = clock64();
   sink[blockIdx.x * blockDim.x + threadIdx.x] = x_or ^ __float_as_uint(l);
-  if (threadIdx.x == 0) out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  if ((threadIdx.x & 31) == 0) out[blockIdx.x * 8 + (threadIdx.x >> 5)] = (unsigned long long)(t1 - t0);
 }
 
 int main() {
   float* d_in; unsigned long long* d_out; uint32_t* d_sink;
-  CK(cudaMalloc(&d_in, 1024 * 4)); CK(cudaMalloc(&d_out, 1024 * 8)); CK(cudaMalloc(&d_sink, 148 * 256 * 4));
+  CK(cudaMalloc(&d_in, 1024 * 4)); CK(cudaMalloc(&d_out, 148 * 8 * 8)); CK(cudaMalloc(&d_sink, 148 * 256 * 4));
   float h[1024]; for (int i = 0; i < 1024; ++i) h[i] = (float)((i * 37) % 101) * 0.05f - 2.5f;
   CK(cudaMemcpy(d_in, h, sizeof(h), cudaMemcpyHostToDevice));
   auto report = [&](const char* name, int threads) {
-    unsigned long long c; CK(cudaMemcpy(&c, d_out, 8, cudaMemcpyDeviceToHost));
-    printf("%-28s warps/SMSP %d : %6.0f cycles per row-block, %6.1f per row per warp\n", name, threads / 128,
-           (double)c / kRows, (double)c / kRows / (threads / 128));
+    unsigned long long c[8]; CK(cudaMemcpy(c, d_out, 64, cudaMemcpyDeviceToHost));
+    unsigned long long lo = c[0], hi = c[0];
+    for (int w = 1; w < threads / 32; ++w) { lo = c[w] < lo ? c[w] : lo; hi = c[w] > hi ? c[w] : hi; }
+    printf("%-28s warps/SMSP %d : first warp %6.0f, last warp %6.0f cycles per row-block -> %6.1f SMSP cycles per 128-col row-warp\n",
+           name, threads / 128, (double)lo / kRows, (double)hi / kRows, (double)hi / kRows / (threads / 128));
   };
 #define RUN(P, K, name)                                                              \
   for (int threads : {128, 256}) {                                                   \

@@ -71,6 +71,13 @@ if VER == "6":
               f"PV0->PV1 (S0 + wait P1) {np.mean(d[:, 1] - d[:, 0]):.0f}, PV1->commits {np.mean(d[:, 13] - d[:, 1]):.0f}, "
               f"S1 issue {np.mean(d[1:, 14] - d[1:, 13]):.0f}; loads lead {np.mean(d[:, 0] - d[:, 7]):.0f}")
     sys.exit(0)
+if os.environ.get("RCP_TRACE_PERWARP"):
+    for cta in (0, 1):
+        d = t[cta, 8:56]
+        base = d[:, 8]
+        print(f"CTA {cta}: P-arrive of softmax warps 4..11 relative to warp 4 (mean over blocks):",
+              " ".join(f"w{4 + w}:{np.mean(d[:, 8 + w] - base):+.0f}" for w in range(8)))
+    sys.exit(0)
 if VER == "5":
     for cta in (0, 1):
         d = t[cta, 8:56]
@@ -78,14 +85,18 @@ if VER == "5":
         s_rdy, p_done = d[:, 2 + 2 * rk], d[:, 3 + 2 * rk]
         print(f"v5 CTA {cta}: cycles/block {np.mean(np.diff(s_rdy)):.0f} (TC ideal 1024 per 128-key block); "
               f"softmax {np.mean(p_done - s_rdy):.0f}; S ready -> next S ready waits {np.mean(s_rdy[1:] - p_done[:-1]):.0f}")
-        print(f"   softmax: S ready -> max exchanged {np.mean(d[:, 12 + rk] - s_rdy):.0f}; "
-              f"last h=0 warp P-arrive - warp4 P-done {np.mean(d[:, 14] - p_done):.0f}; "
-              f"last h=1 warp P-arrive - warp4 P-done {np.mean(d[:, 15] - p_done):.0f}")
+        print(f"   softmax: S ready -> max exchanged {np.mean(d[:, 12 + rk] - s_rdy):.0f}")
+        if rk == 0:
+            print(f"   softmax: P done -> arrive issued {np.mean(d[:, 15] - p_done):.0f}; arrive -> next S seen "
+                  f"{np.mean(s_rdy[1:] - d[:-1, 15]):.0f}")
+        if rk == 0:
+            print(f"   MMA latency (observer warp): S(it) issue end -> S done {np.mean(d[2:, 11] - d[:-2, 10]):.0f}; "
+                  f"PV(it) issue end -> PV done {np.mean(d[:-1, 14] - d[:-1, 8]):.0f}; "
+                  f"S done -> softmax sees it {np.mean(s_rdy - d[:, 11]):.0f}")
         if rk == 0:
             print(f"   leader MMA: P->PV issue {np.mean(d[:, 0] - p_done):.0f}, PV issue {np.mean(d[:, 8] - d[:, 0]):.0f}, "
                   f"commits+wait K {np.mean(d[:, 9] - d[:, 8]):.0f}, S issue {np.mean(d[:, 10] - d[:, 9]):.0f}, "
-                  f"loop top->P wait done {np.mean(d[1:, 0] - d[:-1, 1]):.0f}, loads lead {np.mean(d[:, 0] - d[:, 7]):.0f}; "
-                  f"own last P-arrive -> PV issue {np.mean(d[:, 0] - d[:, 15]):.0f}")
+                  f"loop top->P wait done {np.mean(d[1:, 0] - d[:-1, 1]):.0f}, loads lead {np.mean(d[:, 0] - d[:, 7]):.0f}")
             print(f"   S(it) issued (end of iter it-2) -> S(it) ready at softmax: {np.mean(d[2:, 2] - d[:-2, 10]):.0f}; "
                   f"PV(it-1) issue -> S(it+1) issued: {np.mean(d[1:, 10] - d[:-1, 0]):.0f}")
     sys.exit(0)
