@@ -89,6 +89,22 @@ class StepTrace:
         return "\n".join(lines) + "\n"
 
 
+@dataclass
+class HostStage:
+    """Inputs of one host-buffer prefill staged on the device by
+    ``RingAttention.stage_host_inputs`` (copies queued, with ready events)."""
+
+    plan: ShardPlan
+    kb: EmbeddingBlock
+    vb: EmbeddingBlock
+    q: torch.Tensor
+    qp: torch.Tensor
+    qs: torch.Tensor
+    splits: list
+    kv_ready: torch.cuda.Event
+    q_ready: list
+
+
 # ------------------------------------------------------------------ message layouts
 @dataclass(frozen=True)
 class KvLayout:
@@ -371,52 +387,37 @@ class RingAttention:
             self._bufs[("stream", key)] = s
         return s
 
-    def pass_kv_prefill_host(self, plan: ShardPlan, cache: RankKvCache, q_host, k_host, v_host,
-                             cfg: GqaConfig, out_host: torch.Tensor, lse_host: torch.Tensor,
-                             n_sub: int | None = None) -> None:
-        """Alg. 2 for host-resident inputs and outputs, with the PCIe copies
-        overlapped with the attention.
-
-        q_host/k_host/v_host: per-sequence HOST tensors of the new tokens (pinned
-        for asynchronous copies).  out_host [S, Hq, D] fp32 / lse_host [S, Hq]
-        (pinned) receive this rank's merged result for its S query slots (the
-        rows of ``materialize_rank_block``).  K/V go to the device first (the
-        cache append and the KV message need them), the query slots follow in
-        ``n_sub`` ranges on a copy stream, every ring step runs one attention
-        launch per range, and each range's final rows go back on a second copy
-        stream as soon as its last launch is queued.  Returns when everything
-        is queued; the caller's stream is ordered after the device->host copies.
-        ``n_sub`` defaults to one range per 8192 query slots (about a thousand
-        CTAs per launch), at most 16."""
+    def stage_host_inputs(self, plan: ShardPlan, q_host, k_host, v_host, cfg: GqaConfig, device,
+                          n_sub: int | None = None) -> "HostStage":
+        """Queue the host->device copies of one prefill's inputs on the copy
+        stream: K/V of this rank's chunks first, then its query slots in ranges
+        (``n_sub``, default one per 8192 slots, at most 16), each range with a
+        ready event.  The device buffers come from the copy stream's own pool,
+        so staging may run ahead of the compute stream (e.g. the next request
+        while this one computes); the host tensors must stay unchanged until
+        the copies have run."""
         from .sharding import _host_index_map, materialize_rank_block
 
         k = self.comm.rank
-        dev = cache.device
-        cur = torch.cuda.current_stream(dev)
-        s_in, s_out = self._side_stream("h2d"), self._side_stream("d2h")
+        s_in = self._side_stream("h2d")
         H, D = cfg.n_query_heads, cfg.head_dim
         idx, posv, seqv = _host_index_map(plan, k)
         S = idx.shape[0]
-        # device buffers come from the caller's stream; the copy streams wait
-        # for it first, so no block still in use elsewhere is overwritten
-        q = torch.empty((S, H, D), dtype=torch.bfloat16, device=dev)
-        out = torch.empty((S, H, D), dtype=torch.float32, device=dev)
-        lse = torch.empty((S, H), dtype=torch.float32, device=dev)
-        s_in.wait_stream(cur)
+        if n_sub is None:
+            n_sub = min(16, max(1, S // 8192))
+        step = max(256, -(-S // max(n_sub, 1)) // 256 * 256)
+        splits = [(a, min(S, a + step)) for a in range(0, S, step)]
         with torch.cuda.stream(s_in):
-            kb = materialize_rank_block(plan, k, list(k_host), dev)
-            vb = materialize_rank_block(plan, k, list(v_host), dev)
+            kb = materialize_rank_block(plan, k, list(k_host), device)
+            vb = materialize_rank_block(plan, k, list(v_host), device)
             kv_ready = torch.cuda.Event()
             kv_ready.record(s_in)
-            qp = _lib.h2d(posv.astype(np.int32), dev)
-            qs = _lib.h2d(seqv.astype(np.int32), dev)
+            qp = _lib.h2d(posv.astype(np.int32), device)
+            qs = _lib.h2d(seqv.astype(np.int32), device)
+            q = torch.empty((S, H, D), dtype=torch.bfloat16, device=device)
             srcs = [t.reshape(t.shape[0], -1) for t in q_host]
             seq_off = np.cumsum([0] + [t.shape[0] for t in srcs])  # idx rows are concatenated
             qf = q.view(S, -1)
-            if n_sub is None:
-                n_sub = min(16, max(1, S // 8192))
-            step = max(256, -(-S // max(n_sub, 1)) // 256 * 256)
-            splits = [(a, min(S, a + step)) for a in range(0, S, step)]
             q_ready = []
             for a, b in splits:
                 seg = idx[a:b]
@@ -440,14 +441,50 @@ class RingAttention:
                 ev = torch.cuda.Event()
                 ev.record(s_in)
                 q_ready.append(ev)
-        for t in (kb.data, vb.data, qp, qs):  # made on s_in, read on the caller's stream
+        return HostStage(plan, kb, vb, q, qp, qs, splits, kv_ready, q_ready)
+
+    def join_host_copies(self) -> None:
+        """Order the caller's stream after every queued device->host copy."""
+        torch.cuda.current_stream().wait_stream(self._side_stream("d2h"))
+
+    def pass_kv_prefill_host(self, plan: ShardPlan, cache: RankKvCache, q_host, k_host, v_host,
+                             cfg: GqaConfig, out_host: torch.Tensor, lse_host: torch.Tensor,
+                             n_sub: int | None = None, staged: "HostStage | None" = None,
+                             join: bool = True) -> None:
+        """Alg. 2 for host-resident inputs and outputs, with the PCIe copies
+        overlapped with the attention.
+
+        q_host/k_host/v_host: per-sequence HOST tensors of the new tokens (pinned
+        for asynchronous copies).  out_host [S, Hq, D] fp32 / lse_host [S, Hq]
+        (pinned) receive this rank's merged result for its S query slots (the
+        rows of ``materialize_rank_block``).  The inputs are staged by
+        ``stage_host_inputs`` (or taken from ``staged``, queued earlier), every
+        ring step runs one attention launch per query range as it lands, and
+        each range's final rows go back on a second copy stream as soon as its
+        last launch is queued.  With ``join`` (default) the caller's stream is
+        ordered after those copies; a serving loop that stages the next
+        request meanwhile passes ``join=False`` and calls ``join_host_copies``
+        once at the end."""
+        k = self.comm.rank
+        dev = cache.device
+        cur = torch.cuda.current_stream(dev)
+        s_out = self._side_stream("d2h")
+        st = staged if staged is not None else self.stage_host_inputs(plan, q_host, k_host, v_host, cfg, dev,
+                                                                      n_sub)
+        if st.plan is not plan and st.plan != plan:
+            raise ValueError("staged inputs belong to a different plan")
+        for t in (st.kb.data, st.vb.data, st.q, st.qp, st.qs):  # made on the copy stream, read here
             t.record_stream(cur)
-        cur.wait_event(kv_ready)
-        append_new_tokens(plan, k, cache, kb, vb)
+        H, D = cfg.n_query_heads, cfg.head_dim
+        S = st.q.shape[0]
+        out = torch.empty((S, H, D), dtype=torch.float32, device=dev)
+        lse = torch.empty((S, H), dtype=torch.float32, device=dev)
+        cur.wait_event(st.kv_ready)
+        append_new_tokens(plan, k, cache, st.kb, st.vb)
         lay = KvLayout(kv_message_len(plan), cache.n_kv_heads, cache.head_dim)
         msg = self._buf(("kv", "local"), lay.nbytes, dev)
         build_kv_message(plan, cache, msg)
-        s_out.wait_stream(cur)
+        splits = st.splits
 
         def on_final(i):
             a, b = splits[i]
@@ -458,11 +495,12 @@ class RingAttention:
                 out_host[a:b].copy_(out[a:b], non_blocking=True)
                 lse_host[a:b].copy_(lse[a:b], non_blocking=True)
 
-        self.pass_kv(q, qp, qs, lay, msg, cfg, out, lse, cache.dtype, q_splits=splits, q_ready=q_ready,
-                     on_final=on_final)
+        self.pass_kv(st.q, st.qp, st.qs, lay, msg, cfg, out, lse, cache.dtype, q_splits=splits,
+                     q_ready=st.q_ready, on_final=on_final)
         for t in (out, lse):
             t.record_stream(s_out)
-        cur.wait_stream(s_out)
+        if join:
+            cur.wait_stream(s_out)
 
     def pass_kv_prefill(self, plan: ShardPlan, cache: RankKvCache, q_block: EmbeddingBlock,
                         k_block: EmbeddingBlock, v_block: EmbeddingBlock, cfg: GqaConfig) -> PartialAttention:

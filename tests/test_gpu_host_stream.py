@@ -49,3 +49,46 @@ def test_host_stream_equals_device_path(n_sub, partial):
     torch.cuda.synchronize()
     assert torch.equal(out_h, ref.output.data.cpu())
     assert torch.equal(lse_h, ref.lse.cpu())
+
+
+def test_staged_pipeline_two_requests():
+    """Serving-loop use: request 2 is staged while request 1 computes, the
+    D2H stream is joined once at the end; both results equal the device path."""
+    from paper_2411_01783_b200.attention import GqaConfig
+    from paper_2411_01783_b200.kv_cache import RankKvCache
+    from paper_2411_01783_b200.ring import RingAttention, _LocalComm
+    from paper_2411_01783_b200.sharding import SequenceSpec, materialize_rank_block, plan_full_prefill
+
+    hq, hkv, D = 8, 2, 128
+    cfg = GqaConfig(hq, hkv, D)
+    g = torch.Generator().manual_seed(5)
+    mk = lambda *s: torch.randn(*s, generator=g).to(torch.bfloat16).pin_memory()
+    reqs = []
+    for T in (2048, 1300):
+        plan = plan_full_prefill([SequenceSpec(1, 0, T)], 1)
+        reqs.append((plan, [mk(T, hq, D)], [mk(T, hkv, D)], [mk(T, hkv, D)]))
+    ring = RingAttention(_LocalComm(0, 1))
+    refs = []
+    for plan, qh, kh, vh in reqs:
+        r = ring.pass_kv_prefill(plan, RankKvCache(hkv, D, capacity_tokens=256),
+                                 materialize_rank_block(plan, 0, [qh[0].cuda()]),
+                                 materialize_rank_block(plan, 0, [kh[0].cuda()]),
+                                 materialize_rank_block(plan, 0, [vh[0].cuda()]), cfg)
+        refs.append((r.output.data.cpu(), r.lse.cpu()))
+    torch.cuda.synchronize()
+    outs = []
+    dev = torch.device("cuda")
+    st = ring.stage_host_inputs(reqs[0][0], reqs[0][1], reqs[0][2], reqs[0][3], cfg, dev)
+    for i, (plan, qh, kh, vh) in enumerate(reqs):
+        nxt = ring.stage_host_inputs(*reqs[i + 1], cfg, dev) if i + 1 < len(reqs) else None
+        S = plan.total_query_slots()
+        oh = torch.empty((S, hq, D)).pin_memory()
+        lh = torch.empty((S, hq)).pin_memory()
+        ring.pass_kv_prefill_host(plan, RankKvCache(hkv, D, capacity_tokens=256), qh, kh, vh, cfg, oh, lh,
+                                  staged=st, join=False)
+        outs.append((oh, lh))
+        st = nxt
+    ring.join_host_copies()
+    torch.cuda.synchronize()
+    for (oh, lh), (ro, rl) in zip(outs, refs):
+        assert torch.equal(oh, ro) and torch.equal(lh, rl)
