@@ -75,6 +75,8 @@ struct AttnParams {
   int n_qtiles, n_qblk, n_kblocks;
   int mode;
   float scale_log2;
+  const __nv_bfloat16* q;  // v7: query rows are read directly (into TMEM)
+  int64_t q_stride;        // elements between consecutive query rows
   long long* trace;  // RCP_TRACE builds only: per-CTA role timestamps (clock64)
 };
 
@@ -960,6 +962,357 @@ __global__ void __launch_bounds__(kThreads6, 1) attn_fwd_v6_kernel(const __grid_
 }
 
 // ======================================================================
+// v7: 1-CTA, 64-key blocks, Q in TMEM.  S = Q K^T is a TS MMA (A = the query
+// tile from TMEM, B = K from shared memory): a 128x64 SS MMA needs 6 KB of
+// shared-memory operands per 32 tensor cycles (192 B/clk, runs at 55 %),
+// the TS form only K's 2 KB (64 B/clk, full rate).  TMEM (512 columns):
+// O0 [0,128) | O1 [128,256) | Q0 [256,320) | Q1 [320,384) | S0 [384,448) |
+// S1 [448,512): one S buffer per tile, P_t(j) packed over its first 32
+// columns in two 32-key chunks (PV overlaps the exps), S_t(j+1) issued right
+// after PV_t(j).  The softmax warps write their query rows into TMEM once;
+// Q never touches shared memory, which leaves room for a 14-slot K/V ring.
+// ======================================================================
+constexpr int kSlots7 = 14;
+constexpr uint32_t kSmem7Bytes = kSlots7 * kKVBytes + 1024;
+constexpr uint32_t kTmemO7 = 0, kTmemQ7 = 256, kTmemS7 = 384;
+static_assert(kSmem7Bytes <= 232448, "v7 shared memory exceeds 227 KB");
+
+__global__ void __launch_bounds__(kThreads, 1) attn_fwd_v7_kernel(const __grid_constant__ AttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem =
+      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sKV = smem;  // kSlots7 K/V blocks (16 KB each)
+
+  __shared__ uint64_t bar_full[kSlots7], bar_empty[kSlots7];
+  __shared__ uint64_t bar_qt[2], bar_s[2], bar_p[2][2], bar_o[2];
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = static_cast<int>(warp_id());
+  const int per_kv = p.n_qblk * p.group;
+  const int kvh = static_cast<int>(blockIdx.x) / per_kv;
+  const int rem = static_cast<int>(blockIdx.x) - kvh * per_kv;
+  const int qblk = p.n_qblk - 1 - rem / p.group;
+  const int head = kvh * p.group + rem % p.group;
+  const int n = __ldg(p.act_n + qblk);
+  const uint32_t* act = p.act + static_cast<int64_t>(qblk) * p.n_kblocks;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSlots7; ++s) {
+      mbar_init(&bar_full[s], 1);
+      mbar_init(&bar_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&bar_qt[t], 128);
+      mbar_init(&bar_s[t], 1);
+      mbar_init(&bar_p[t][0], 128);
+      mbar_init(&bar_p[t][1], 128);
+      mbar_init(&bar_o[t], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (K_j, V_j)
+    if (elect_one() && n > 0) {
+      tma_prefetch_desc(&p.tm_k);
+      tma_prefetch_desc(&p.tm_v);
+      const uint64_t pol_kv = policy_evict_last();
+      uint32_t ld = 0;
+      uint32_t e_next = __ldg(act);
+      for (int it = 0; it < n; ++it) {
+        const int j = act_j(e_next);
+        if (it + 1 < n) e_next = __ldg(act + it + 1);
+#pragma unroll
+        for (int kv = 0; kv < 2; ++kv, ++ld) {
+          const uint32_t slot = ld % kSlots7, ph = (ld / kSlots7) & 1;
+          mbar_wait(&bar_empty[slot], ph ^ 1);
+          TRACE(6 + kv, it);
+          mbar_arrive_expect_tx(&bar_full[slot], kKVBytes);
+          const CUtensorMap* map = kv ? &p.tm_v : &p.tm_k;
+          for (int h = 0; h < 2; ++h)
+            tma_load_2d(sKV + slot * kKVBytes + h * kKVBoxBytes, map, &bar_full[slot], kvh * kD + h * 64,
+                        j * kKRows, pol_kv);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (one elected lane)
+    if (elect_one() && n > 0) {
+      const uint32_t idesc_s = make_idesc_bf16_f32(kQRows, kKRows, 0, 0);
+      const uint32_t idesc_o = make_idesc_bf16_f32(kQRows, kD, 0, 1);
+      const uint32_t k_lo = sw128_desc_lo(smem_u32(sKV), 16);
+      const uint32_t v_lo = sw128_desc_lo(smem_u32(sKV), kKVBoxBytes);
+      auto wait_load = [&](uint32_t ld) {
+        mbar_wait(&bar_full[ld % kSlots7], (ld / kSlots7) & 1);
+        tc_fence_after();
+      };
+      auto issue_s = [&](int t, uint32_t ld) {  // TS: A = Q_t in TMEM, B = K (K-major)
+        const uint32_t ka = k_lo + (((ld % kSlots7) * kKVBytes) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk)
+          mma_ts_lo(tmem + kTmemS7 + t * kKRows, tmem + kTmemQ7 + t * 64 + kk * 8,
+                    ka + (((kk >> 2) * kKVBoxBytes + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
+      };
+      auto issue_pv = [&](int t, uint32_t ld, int it) {  // two 32-key chunks as P lands
+        const uint32_t va = v_lo + (((ld % kSlots7) * kKVBytes) >> 4);
+        const uint32_t pa = tmem + kTmemS7 + t * kKRows;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          mbar_wait(&bar_p[t][q], it & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 2 * q; kk < 2 * q + 2; ++kk)
+            mma_ts_lo(tmem + kTmemO7 + t * kD, pa + kk * 8, va + ((kk * 2048) >> 4), idesc_o,
+                      (it > 0 || kk > 0) ? 1u : 0u);
+        }
+      };
+      mbar_wait(&bar_qt[0], 0);
+      mbar_wait(&bar_qt[1], 0);
+      tc_fence_after();
+      wait_load(0);
+      issue_s(0, 0);
+      mma_commit(&bar_s[0]);
+      issue_s(1, 0);
+      mma_commit(&bar_s[1]);
+      mma_commit(&bar_empty[0]);
+      for (int it = 0; it < n; ++it) {
+        const bool last = it + 1 == n;
+        const uint32_t ldv = 2 * it + 1, ldk1 = 2 * it + 2;
+        wait_load(ldv);
+        issue_pv(0, ldv, it);
+        TRACE(0, it);
+        if (last) mma_commit(&bar_o[0]);
+        if (!last) {
+          wait_load(ldk1);
+          issue_s(0, ldk1);
+          mma_commit(&bar_s[0]);
+        }
+        issue_pv(1, ldv, it);
+        TRACE(1, it);
+        if (last) mma_commit(&bar_o[1]);
+        mma_commit(&bar_empty[ldv % kSlots7]);
+        if (!last) {
+          issue_s(1, ldk1);
+          mma_commit(&bar_s[1]);
+          mma_commit(&bar_empty[ldk1 % kSlots7]);
+        }
+        TRACE(14, it);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax + epilogue
+    const int w = (warp - 4) >> 2;                                 // query tile 0 / 1
+    const int t = static_cast<int>(threadIdx.x) - 128 - 128 * w;  // row inside the tile
+    const int row = (2 * qblk + w) * kQRows + t;
+    const bool row_ok = row < p.tq;
+    const int my_pos = row_ok ? __ldg(p.q_pos + row) : -1;
+    const int my_seq = row_ok ? __ldg(p.q_seq + row) : RCP_SEQ_PAD_Q;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+    const uint32_t o_addr = lane_base + kTmemO7 + w * kD;
+    const uint32_t s_addr = lane_base + kTmemS7 + w * kKRows;
+    // this row of Q into TMEM (A operand layout: column c holds dims 2c, 2c+1)
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(p.q + static_cast<int64_t>(row) * p.q_stride + head * kD);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint32_t r[32];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint4 v = row_ok && n > 0 ? __ldg(src + half * 8 + i) : make_uint4(0, 0, 0, 0);
+          r[4 * i] = v.x;
+          r[4 * i + 1] = v.y;
+          r[4 * i + 2] = v.z;
+          r[4 * i + 3] = v.w;
+        }
+        tmem_st32(lane_base + kTmemQ7 + w * 64 + half * 32, r);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bar_qt[w]);
+    }
+    const float sl2 = p.scale_log2;
+    const uint64_t sl2x2 = f2(sl2, sl2);
+    float m = -INFINITY, l = 0.f;
+    uint32_t e_next = n > 0 ? __ldg(act) : 0u;
+    int it = 0;
+    for (; it < n; ++it) {
+      const uint32_t e = e_next;
+      if (it + 1 < n) e_next = __ldg(act + it + 1);
+      const int j = act_j(e);
+      const int cls = act_cls(e, w);
+      // S_t(it) complete also means PV_t(it-1) is: O_t may be rescaled in place.
+      mbar_wait(&bar_s[w], it & 1);
+      tc_fence_after();
+      if (t == 0) TRACE(2 + 2 * w, it);
+      if (cls != kTileEmpty) {  // warp-uniform
+        uint32_t sr[64];
+        tmem_ld32(s_addr, sr);
+        tmem_ld32(s_addr + 32, sr + 32);
+        tmem_ld_wait();
+        float s[64];
+#pragma unroll
+        for (int c = 0; c < 64; ++c) s[c] = __uint_as_float(sr[c]);
+        if (cls == kTilePartial) {
+          const int base = j * kKRows;
+          if (base + kKRows <= p.tk) {
+            const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + base);
+            const int4* ks4 = reinterpret_cast<const int4*>(p.k_seq + base);
+#pragma unroll
+            for (int c4 = 0; c4 < 16; ++c4) {
+              const int4 kp = __ldg(kp4 + c4), kq = __ldg(ks4 + c4);
+              if (!(kq.x == my_seq && kp.x <= my_pos)) s[4 * c4 + 0] = -INFINITY;
+              if (!(kq.y == my_seq && kp.y <= my_pos)) s[4 * c4 + 1] = -INFINITY;
+              if (!(kq.z == my_seq && kp.z <= my_pos)) s[4 * c4 + 2] = -INFINITY;
+              if (!(kq.w == my_seq && kp.w <= my_pos)) s[4 * c4 + 3] = -INFINITY;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 64; ++c) {
+              const int kidx = base + c;
+              const bool ok = kidx < p.tk && __ldg(p.k_seq + kidx) == my_seq &&
+                              __ldg(p.k_pos + kidx) <= my_pos;
+              if (!ok) s[c] = -INFINITY;
+            }
+          }
+        }
+        float m8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m8[k] = fmaxf(s[k], s[8 + k]);
+#pragma unroll
+        for (int c = 16; c < 64; c += 8)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m8[k] = fmaxf(m8[k], s[c + k]);
+        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        const float m_old = m;
+        const float m_new = fmaxf(m, mx * sl2);
+        const bool need = m_new > m + kRescaleThreshold;  // also true for -inf -> finite
+        if (need) m = m_new;
+        const float m_use = (m == -INFINITY) ? 0.f : m;
+        const uint64_t negm2 = f2(-m_use, -m_use);
+        const float f = (need && m_old != -INFINITY) ? ex2_approx(m_old - m) : 1.0f;
+        if (__any_sync(0xffffffffu, f != 1.0f && it > 0)) {
+#pragma unroll 1
+          for (int c = 0; c < kD; c += 32) {
+            uint32_t r[32];
+            tmem_ld32(o_addr + c, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
+            tmem_st32(o_addr + c, r);
+          }
+        }
+        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {  // P chunk q: keys [32q, 32q+32) -> columns [16q, 16q+16)
+          uint32_t pk[16];
+          if (cls == kTileFull) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int ip = 16 * q + i;
+              const float2 x = unf2(ffma2(f2(s[2 * ip], s[2 * ip + 1]), sl2x2, negm2));
+              float p0, p1;
+              if ((ip & 7) < kPolyPairsPer8) {
+                p0 = ex2_poly(x.x);
+                p1 = ex2_poly(x.y);
+              } else {
+                p0 = ex2_approx(x.x);
+                p1 = ex2_approx(x.y);
+              }
+              acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
+              pk[i] = pack_bf16x2(p0, p1);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int ip = 16 * q + i;
+              const float2 x = unf2(ffma2(f2(s[2 * ip], s[2 * ip + 1]), sl2x2, negm2));
+              const float p0 = ex2_approx(x.x), p1 = ex2_approx(x.y);
+              acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
+              pk[i] = pack_bf16x2(p0, p1);
+            }
+          }
+          tmem_st16(s_addr + 16 * q, pk);
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&bar_p[w][q]);
+        }
+        const float2 a01 = unf2(fadd2(acc2[0], acc2[1]));
+        const float2 a23 = unf2(fadd2(acc2[2], acc2[3]));
+        const float sum = (a01.x + a01.y) + (a23.x + a23.y);
+        l = (m_old == -INFINITY ? 0.f : l * f) + sum;
+      } else {
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pk[i] = 0u;
+        tmem_st32(s_addr, pk);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&bar_p[w][0]);
+        mbar_arrive(&bar_p[w][1]);
+      }
+      if (t == 0) TRACE(3 + 2 * w, it);
+    }
+
+    // epilogue: O / l, LSE, optional merge into the running (O, LSE)
+    if (it > 0) {
+      mbar_wait(&bar_o[w], 0);
+      tc_fence_after();
+    }
+    const bool merge = p.mode == RCP_MODE_MERGE;
+    if (!(merge && it == 0)) {
+      const bool has = l > 0.f;
+      const float inv = has ? 1.0f / l : 0.f;
+      const float lse_new = has ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+      float* orow = p.o + (static_cast<int64_t>(row) * p.hq + head) * kD;
+      float* lrow = p.lse + static_cast<int64_t>(row) * p.hq + head;
+      MergeW mw;
+      mw.lse = lse_new;
+      mw.wa = 0.f;
+      mw.wb = 1.f;
+      if (merge && row_ok) mw = merge_weights(__ldg(lrow), lse_new);
+#pragma unroll
+      for (int c = 0; c < kD; c += 32) {
+        uint32_t r[32];
+        if (it > 0) {
+          tmem_ld32(o_addr + c, r);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+        if (row_ok) {
+          float4* dst = reinterpret_cast<float4*>(orow + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float4 v = make_float4(__uint_as_float(r[4 * i]) * inv, __uint_as_float(r[4 * i + 1]) * inv,
+                                   __uint_as_float(r[4 * i + 2]) * inv,
+                                   __uint_as_float(r[4 * i + 3]) * inv);
+            if (merge) {
+              const float4 a = dst[i];
+              v = make_float4(merge_val(a.x, v.x, mw), merge_val(a.y, v.y, mw),
+                              merge_val(a.z, v.z, mw), merge_val(a.w, v.w, mw));
+            }
+            dst[i] = v;
+          }
+        }
+      }
+      if (row_ok) *lrow = merge ? mw.lse : lse_new;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// ======================================================================
 // v5: CTA-pair (cta_group::2) variant.  Cluster of 2 CTAs = 2 x 128 query rows
 // of one query head (CTA r owns query tile 2*qblk + r).  Key blocks are 128
 // keys; the leader CTA issues M=256 MMAs: S = Q K^T (N=128 keys, B split by
@@ -1533,15 +1886,16 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
 
   // v4 (1-CTA, 64-key blocks) is the default: it measured best on the power-
   // capped B200s ("Attention kernel versions").  RCP_ATTN_VERSION=5
-  // (CTA pairs) and =6 (1-CTA, 128-key blocks, split softmax) are kept for
+  // (CTA pairs), =6 (1-CTA, 128-key blocks, split softmax) and =7 (Q in TMEM,
+  // TS-form S) are kept for
   // A/B measurements; all three pass the same parity tests.
   static int version = -1;
   if (version < 0) {
     const char* e = getenv("RCP_ATTN_VERSION");
     const int v = e ? atoi(e) : 4;
-    version = (v == 5 || v == 6) ? v : 4;
+    version = (v == 5 || v == 6 || v == 7) ? v : 4;
   }
-  const int krows = version == 4 ? kKRows : kKRows6;
+  const int krows = (version == 4 || version == 7) ? kKRows : kKRows6;
   AttnParams prm;
   memset(&prm, 0, sizeof(prm));
   int rc;
@@ -1551,8 +1905,10 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
                      version == 6 ? kKRows6 : kKRows)) != RCP_OK)
     return rc;
   if ((rc = make_map(&prm.tm_v, v, tk, static_cast<int64_t>(hkv) * kD, v_row_stride,
-                     version == 4 ? kKRows : kKRows2)) != RCP_OK)
+                     (version == 4 || version == 7) ? kKRows : kKRows2)) != RCP_OK)
     return rc;
+  prm.q = static_cast<const __nv_bfloat16*>(q);
+  prm.q_stride = q_row_stride;
   TileSum* qsum = static_cast<TileSum*>(workspace);
   const int n_qtiles = static_cast<int>((tq + kQRows - 1) / kQRows);
   const int n_kblocks = static_cast<int>((tk + krows - 1) / krows);
@@ -1598,6 +1954,14 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
       attr2 = true;
     }
     attn_fwd_2cta_kernel<<<static_cast<unsigned>(2 * grid), kThreads2, kSmem2Bytes, st>>>(prm);
+  } else if (version == 7) {
+    static bool attr7 = false;
+    if (!attr7) {
+      RCP_CUDA(cudaFuncSetAttribute(attn_fwd_v7_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kSmem7Bytes));
+      attr7 = true;
+    }
+    attn_fwd_v7_kernel<<<static_cast<unsigned>(grid), kThreads, kSmem7Bytes, st>>>(prm);
   } else if (version == 6) {
     static bool attr6 = false;
     if (!attr6) {
