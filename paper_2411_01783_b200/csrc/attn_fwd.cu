@@ -1887,8 +1887,7 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
   // v4 (1-CTA, 64-key blocks) is the default: it measured best on the power-
   // capped B200s ("Attention kernel versions").  RCP_ATTN_VERSION=5
   // (CTA pairs), =6 (1-CTA, 128-key blocks, split softmax) and =7 (Q in TMEM,
-  // TS-form S) are kept for
-  // A/B measurements; all three pass the same parity tests.
+  // TS-form S) are kept for A/B measurements; all pass the same parity tests.
   static int version = -1;
   if (version < 0) {
     const char* e = getenv("RCP_ATTN_VERSION");
