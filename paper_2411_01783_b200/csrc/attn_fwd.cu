@@ -1791,6 +1791,364 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   }
 }
 
+// ======================================================================
+// v8: CTA pairs (as v5: M=256 MMAs, 128-key blocks, B split across the
+// pair), but the two softmax warpgroups of a CTA take ALTERNATE key blocks
+// instead of splitting every block's columns: group x owns blocks it ≡ x
+// (mod 2) with full 128-column rows (no per-block row-max exchange), its own
+// S buffer and its own O accumulator and (m, l); the two partials are folded
+// once in the epilogue with the exact LSE merge.  TMEM per CTA: O_a [0,128) |
+// O_b [128,256) | S_a [256,384) | S_b [384,512).  While one group's
+// PV -> S(next) chain runs on the tensor cores, the other group's softmax
+// keeps the SMSPs busy.
+// ======================================================================
+constexpr uint32_t kTmemO8 = 0, kTmemS8 = 256;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    attn_fwd_v8_kernel(const __grid_constant__ AttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem =
+      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                  // this CTA's 128-row query tile
+  uint8_t* sKV = smem + kQTileBytes;   // kSlots2 half blocks (K half / V half alternate)
+
+  __shared__ uint64_t bar_q, bar_full[kSlots2], bar_empty[kSlots2];
+  __shared__ uint64_t bar_s[2], bar_p[2], bar_o[2];
+  __shared__ uint32_t tmem_slot;
+  __shared__ float xch8[2][2][128];  // [group][m | l][row]
+
+  const int warp = static_cast<int>(warp_id());
+  const int rank = static_cast<int>(cluster_rank());
+  const int pair = static_cast<int>(blockIdx.x) >> 1;
+  const int per_kv = p.n_qblk * p.group;
+  const int kvh = pair / per_kv;
+  const int rem = pair - kvh * per_kv;
+  const int qblk = p.n_qblk - 1 - rem / p.group;
+  const int head = kvh * p.group + rem % p.group;
+  const int n = __ldg(p.act_n + qblk);
+  const uint32_t* act = p.act + static_cast<int64_t>(qblk) * p.n_kblocks;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_q, 1);
+    for (int s = 0; s < kSlots2; ++s) {
+      mbar_init(&bar_full[s], 1);
+      mbar_init(&bar_empty[s], 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&bar_s[x], 1);
+      mbar_init(&bar_p[x], 2 * 4);  // the 4 warps of group x in both CTAs
+      mbar_init(&bar_o[x], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                 "n"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (elect_one() && n > 0) {
+      tma_prefetch_desc(&p.tm_q);
+      tma_prefetch_desc(&p.tm_k);
+      tma_prefetch_desc(&p.tm_v);
+      const uint64_t pol_q = policy_evict_first();
+      const uint64_t pol_kv = policy_evict_last();
+      if (rank == 0) mbar_arrive_expect_tx(&bar_q, 2 * kQTileBytes);
+      for (int h = 0; h < 2; ++h)
+        tma_load_2d_pair(sQ + h * kQBoxBytes, &p.tm_q, &bar_q, head * kD + h * 64,
+                         (2 * qblk + rank) * kQRows, pol_q);
+      uint32_t ld = 0;
+      uint32_t e_next = __ldg(act);
+      for (int it = 0; it < n; ++it) {
+        const int j = act_j(e_next);
+        if (it + 1 < n) e_next = __ldg(act + it + 1);
+#pragma unroll
+        for (int kv = 0; kv < 2; ++kv, ++ld) {
+          const uint32_t slot = ld % kSlots2, ph = (ld / kSlots2) & 1;
+          mbar_wait(&bar_empty[slot], ph ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&bar_full[slot], 2 * kSlot2Bytes);
+          uint8_t* dst = sKV + slot * kSlot2Bytes;
+          if (kv == 0) {  // K half: keys [j*128 + 64 r, +64), all 128 dims (two 8 KB boxes)
+            for (int h = 0; h < 2; ++h)
+              tma_load_2d_pair(dst + h * 8192, &p.tm_k, &bar_full[slot], kvh * kD + h * 64,
+                               j * kKRows2 + rank * 64, pol_kv);
+          } else {        // V half: all 128 keys, dims [64 r, 64 r + 64)
+            tma_load_2d_pair(dst, &p.tm_v, &bar_full[slot], kvh * kD + rank * 64, j * kKRows2, pol_kv);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA, one elected lane)
+    if (rank == 0 && n > 0 && elect_one()) {
+      const uint32_t idesc_s = make_idesc_bf16_f32(256, kKRows2, 0, 0);
+      const uint32_t idesc_o = make_idesc_bf16_f32(256, kD, 0, 1);
+      const uint32_t q_lo = sw128_desc_lo(smem_u32(sQ), 16);
+      const uint32_t k_lo = sw128_desc_lo(smem_u32(sKV), 16);
+      const uint32_t v_lo = sw128_desc_lo(smem_u32(sKV), kSlot2Bytes);
+      auto wait_load = [&](uint32_t ld) {
+        mbar_wait(&bar_full[ld % kSlots2], (ld / kSlots2) & 1);
+        tc_fence_after();
+      };
+      auto issue_s = [&](int x, uint32_t ld) {
+        const uint32_t ka = k_lo + (((ld % kSlots2) * kSlot2Bytes) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk)
+          mma2_ss_lo(tmem + kTmemS8 + x * 128, q_lo + (((kk >> 2) * kQBoxBytes + (kk & 3) * 32) >> 4),
+                     ka + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
+      };
+      auto issue_pv = [&](int x, uint32_t ld, bool acc) {
+        const uint32_t va = v_lo + (((ld % kSlots2) * kSlot2Bytes) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < kKRows2 / 16; ++kk)
+          mma2_ts_lo(tmem + kTmemO8 + x * kD, tmem + kTmemS8 + x * 128 + kk * 8, va + ((kk * 2048) >> 4),
+                     idesc_o, (acc || kk > 0) ? 1u : 0u);
+      };
+      mbar_wait(&bar_q, 0);
+      for (int b = 0; b < 2 && b < n; ++b) {
+        wait_load(2 * b);
+        issue_s(b, 2 * b);
+        commit2_mc(&bar_s[b]);
+        commit2_mc(&bar_empty[(2 * b) % kSlots2]);
+      }
+      for (int it = 0; it < n; ++it) {
+        const int x = it & 1;
+        const uint32_t ldv = 2 * it + 1, ldk2 = 2 * (it + 2);
+        wait_load(ldv);
+        mbar_wait(&bar_p[x], (it >> 1) & 1);
+        tc_fence_after();
+        TRACE(0, it);
+        issue_pv(x, ldv, it >= 2);
+        if (it + 2 >= n) commit2_mc(&bar_o[x]);  // last block of group x
+        commit2_mc(&bar_empty[ldv % kSlots2]);
+        if (it + 2 < n) {
+          wait_load(ldk2);
+          issue_s(x, ldk2);
+          commit2_mc(&bar_s[x]);
+          commit2_mc(&bar_empty[ldk2 % kSlots2]);
+        }
+        TRACE(1, it);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax (group x: blocks x, x+2, ...)
+    const int x = (warp - 4) >> 2;
+    const int t = static_cast<int>(threadIdx.x) - 128 - 128 * x;  // row inside this CTA's tile
+    const int row = (2 * qblk + rank) * kQRows + t;
+    const bool row_ok = row < p.tq;
+    const int my_pos = row_ok ? __ldg(p.q_pos + row) : -1;
+    const int my_seq = row_ok ? __ldg(p.q_seq + row) : RCP_SEQ_PAD_Q;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+    const uint32_t s_addr = lane_base + kTmemS8 + x * 128;
+    const float sl2 = p.scale_log2;
+    const uint64_t sl2x2 = f2(sl2, sl2);
+    float m = -INFINITY, l = 0.f;
+    int cnt = 0;  // blocks processed by this group
+    for (int it = x; it < n; it += 2, ++cnt) {
+      const uint32_t e = __ldg(act + it);
+      const int j = act_j(e);
+      const int cls = act_cls(e, rank);
+      // S_x(it) complete also means PV_x(it-2) is: O_x may be rescaled in place.
+      mbar_wait(&bar_s[x], cnt & 1);
+      tc_fence_after();
+      if (t == 0) TRACE(2 + 2 * x, it);
+      if (cls != kTileEmpty) {  // uniform across the pair for this block
+        float s[128];
+        {
+          uint32_t sr[128];
+#pragma unroll
+          for (int c = 0; c < 128; c += 32) tmem_ld32(s_addr + c, sr + c);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < 128; ++c) s[c] = __uint_as_float(sr[c]);
+        }
+        if (cls == kTilePartial) {
+          const int base = j * kKRows2;
+          if (base + kKRows2 <= p.tk) {
+            const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + base);
+            const int4* ks4 = reinterpret_cast<const int4*>(p.k_seq + base);
+#pragma unroll
+            for (int c4 = 0; c4 < 32; ++c4) {
+              const int4 kp = __ldg(kp4 + c4), kq = __ldg(ks4 + c4);
+              if (!(kq.x == my_seq && kp.x <= my_pos)) s[4 * c4 + 0] = -INFINITY;
+              if (!(kq.y == my_seq && kp.y <= my_pos)) s[4 * c4 + 1] = -INFINITY;
+              if (!(kq.z == my_seq && kp.z <= my_pos)) s[4 * c4 + 2] = -INFINITY;
+              if (!(kq.w == my_seq && kp.w <= my_pos)) s[4 * c4 + 3] = -INFINITY;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 128; ++c) {
+              const int kidx = base + c;
+              const bool ok = kidx < p.tk && __ldg(p.k_seq + kidx) == my_seq &&
+                              __ldg(p.k_pos + kidx) <= my_pos;
+              if (!ok) s[c] = -INFINITY;
+            }
+          }
+        }
+        float m8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m8[k] = fmaxf(s[k], s[8 + k]);
+#pragma unroll
+        for (int c = 16; c < 128; c += 8)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m8[k] = fmaxf(m8[k], s[c + k]);
+        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        const float m_old = m;
+        const float m_new = fmaxf(m, mx * sl2);
+        const bool need = m_new > m + kRescaleThreshold;  // also true for -inf -> finite
+        if (need) m = m_new;
+        const float m_use = (m == -INFINITY) ? 0.f : m;
+        const uint64_t negm2 = f2(-m_use, -m_use);
+        const float f = (need && m_old != -INFINITY) ? ex2_approx(m_old - m) : 1.0f;
+        if (__any_sync(0xffffffffu, f != 1.0f && cnt > 0)) {
+          const uint32_t o_x = lane_base + kTmemO8 + x * kD;
+#pragma unroll 1
+          for (int c = 0; c < kD; c += 16) {
+            uint32_t r[16];
+            tmem_ld16(o_x + c, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
+            tmem_st16(o_x + c, r);
+          }
+        }
+        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // 32 keys -> 16 packed columns per chunk
+          uint32_t pk[16];
+          if (cls == kTileFull) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int ip = 16 * q + i;
+              const float2 xx = unf2(ffma2(f2(s[2 * ip], s[2 * ip + 1]), sl2x2, negm2));
+              float p0, p1;
+              if ((ip & 7) < kPolyPairsPer8) {
+                p0 = ex2_poly(xx.x);
+                p1 = ex2_poly(xx.y);
+              } else {
+                p0 = ex2_approx(xx.x);
+                p1 = ex2_approx(xx.y);
+              }
+              acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
+              pk[i] = pack_bf16x2(p0, p1);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int ip = 16 * q + i;
+              const float2 xx = unf2(ffma2(f2(s[2 * ip], s[2 * ip + 1]), sl2x2, negm2));
+              const float p0 = ex2_approx(xx.x), p1 = ex2_approx(xx.y);
+              acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
+              pk[i] = pack_bf16x2(p0, p1);
+            }
+          }
+          tmem_st16(s_addr + 16 * q, pk);
+        }
+        const float2 a01 = unf2(fadd2(acc2[0], acc2[1]));
+        const float2 a23 = unf2(fadd2(acc2[2], acc2[3]));
+        const float sum = (a01.x + a01.y) + (a23.x + a23.y);
+        l = (m_old == -INFINITY ? 0.f : l * f) + sum;
+      } else {
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pk[i] = 0u;
+        tmem_st32(s_addr, pk);
+        tmem_st32(s_addr + 32, pk);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      if (t == 0) TRACE(3 + 2 * x, it);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) arrive_leader(&bar_p[x]);
+    }
+
+    // epilogue: fold the two groups' partials (exact LSE merge), O / l, LSE, optional merge
+    const bool has_a = n > 0, has_b = n > 1;
+    if (has_a) {
+      mbar_wait(&bar_o[0], 0);
+      if (has_b) mbar_wait(&bar_o[1], 0);
+      tc_fence_after();
+    }
+    const bool merge = p.mode == RCP_MODE_MERGE;
+    xch8[x][0][t] = m;
+    xch8[x][1][t] = l;
+    named_bar_sync(1 + (warp & 3), 64);  // warps w and w+4 share rows
+    const float ma = xch8[0][0][t], la = xch8[0][1][t];
+    const float mb = xch8[1][0][t], lb = xch8[1][1][t];
+    if (!(merge && n == 0)) {
+      const float mt = fmaxf(ma, mb);
+      const float fa = (ma == -INFINITY) ? 0.f : ex2_approx(ma - mt);
+      const float fb = (mb == -INFINITY) ? 0.f : ex2_approx(mb - mt);
+      const float lt = la * fa + lb * fb;
+      const bool has = lt > 0.f;
+      const float inv = has ? 1.0f / lt : 0.f;
+      const float lse_new = has ? (mt + __log2f(lt)) * 0.69314718055994530942f : -INFINITY;
+      // group x writes output columns [64x, 64x + 64)
+      float* orow = p.o + (static_cast<int64_t>(row) * p.hq + head) * kD + x * 64;
+      float* lrow = p.lse + static_cast<int64_t>(row) * p.hq + head;
+      MergeW mw;
+      mw.lse = lse_new;
+      mw.wa = 0.f;
+      mw.wb = 1.f;
+      if (merge && row_ok) mw = merge_weights(__ldg(lrow), lse_new);
+      const float wa = fa * inv, wb = fb * inv;
+#pragma unroll
+      for (int c = 0; c < 64; c += 32) {
+        uint32_t ra[32], rb[32];
+        if (has_a) {
+          tmem_ld32(lane_base + kTmemO8 + x * 64 + c, ra);
+          if (has_b) tmem_ld32(lane_base + kTmemO8 + kD + x * 64 + c, rb);
+          tmem_ld_wait();
+        }
+        if (!has_a) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ra[i] = 0u;
+        }
+        if (!has_b) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) rb[i] = 0u;
+        }
+        if (row_ok) {
+          float4* dst = reinterpret_cast<float4*>(orow + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float4 v;
+            v.x = __uint_as_float(ra[4 * i]) * wa + __uint_as_float(rb[4 * i]) * wb;
+            v.y = __uint_as_float(ra[4 * i + 1]) * wa + __uint_as_float(rb[4 * i + 1]) * wb;
+            v.z = __uint_as_float(ra[4 * i + 2]) * wa + __uint_as_float(rb[4 * i + 2]) * wb;
+            v.w = __uint_as_float(ra[4 * i + 3]) * wa + __uint_as_float(rb[4 * i + 3]) * wb;
+            if (merge) {
+              const float4 a = dst[i];
+              v = make_float4(merge_val(a.x, v.x, mw), merge_val(a.y, v.y, mw), merge_val(a.z, v.z, mw),
+                              merge_val(a.w, v.w, mw));
+            }
+            dst[i] = v;
+          }
+        }
+      }
+      if (merge) named_bar_sync(1 + (warp & 3), 64);  // both groups read the old LSE before it is overwritten
+      if (row_ok && x == 0) *lrow = merge ? mw.lse : lse_new;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer's TMEM / smem stay live until the leader's MMAs are done
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512) : "memory");
+  }
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1886,13 +2244,14 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
 
   // v4 (1-CTA, 64-key blocks) is the default: it measured best on the power-
   // capped B200s ("Attention kernel versions").  RCP_ATTN_VERSION=5
-  // (CTA pairs), =6 (1-CTA, 128-key blocks, split softmax) and =7 (Q in TMEM,
-  // TS-form S) are kept for A/B measurements; all pass the same parity tests.
+  // (CTA pairs), =6 (1-CTA, 128-key blocks, split softmax), =7 (Q in TMEM,
+  // TS-form S) and =8 (CTA pairs, alternate-block softmax groups) are kept for
+  // A/B measurements; all pass the same parity tests.
   static int version = -1;
   if (version < 0) {
     const char* e = getenv("RCP_ATTN_VERSION");
     const int v = e ? atoi(e) : 4;
-    version = (v == 5 || v == 6 || v == 7) ? v : 4;
+    version = (v == 5 || v == 6 || v == 7 || v == 8) ? v : 4;
   }
   const int krows = (version == 4 || version == 7) ? kKRows : kKRows6;
   AttnParams prm;
@@ -1945,7 +2304,15 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
 
   const int64_t grid = static_cast<int64_t>(prm.n_qblk) * hq;
   RCP_CHECK_ARG(grid < (1ll << 30), "grid too large");
-  if (version == 5) {
+  if (version == 8) {
+    static bool attr8 = false;
+    if (!attr8) {
+      RCP_CUDA(cudaFuncSetAttribute(attn_fwd_v8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kSmem2Bytes));
+      attr8 = true;
+    }
+    attn_fwd_v8_kernel<<<static_cast<unsigned>(2 * grid), kThreads, kSmem2Bytes, st>>>(prm);
+  } else if (version == 5) {
     static bool attr2 = false;
     if (!attr2) {
       RCP_CUDA(cudaFuncSetAttribute(attn_fwd_2cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -71,6 +71,19 @@ if VER == "6":
               f"PV0->PV1 (S0 + wait P1) {np.mean(d[:, 1] - d[:, 0]):.0f}, PV1->commits {np.mean(d[:, 13] - d[:, 1]):.0f}, "
               f"S1 issue {np.mean(d[1:, 14] - d[1:, 13]):.0f}; loads lead {np.mean(d[:, 0] - d[:, 7]):.0f}")
     sys.exit(0)
+if VER == "8":
+    for cta in (0, 1):
+        d = t[cta]
+        for x in (0, 1):
+            its = np.arange(8 + x, 56, 2)
+            s_seen, p_done = d[its, 2 + 2 * x], d[its, 3 + 2 * x]
+            print(f"v8 CTA {cta} group {x}: cycles per own block {np.mean(np.diff(s_seen)):.0f} "
+                  f"(2 blocks of the pair per period; TC ideal 2 x 1024); softmax {np.mean(p_done - s_seen):.0f}; "
+                  f"P done -> next own S seen {np.mean(s_seen[1:] - p_done[:-1]):.0f}")
+        if cta == 0:
+            its = np.arange(8, 56)
+            print(f"   leader: P(it) wait done -> PV issued {np.mean(d[its, 1] - d[its, 0]):.0f} (PV+S issue incl. K wait)")
+    sys.exit(0)
 if os.environ.get("RCP_TRACE_PERWARP"):
     for cta in (0, 1):
         d = t[cta, 8:56]
