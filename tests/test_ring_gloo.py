@@ -168,7 +168,7 @@ def _worker(rank, world, port, T, hq, hkv, errq):
         raise
 
 
-@pytest.mark.parametrize("world,T,hq,hkv", [(2, 64, 4, 2), (3, 50, 4, 1)])
+@pytest.mark.parametrize("world,T,hq,hkv", [(2, 64, 4, 2), (3, 50, 4, 1), (8, 150, 4, 2)])
 def test_ring_spmd_gloo(world, T, hq, hkv):
     ctx = mp.get_context("spawn")
     errq = ctx.SimpleQueue()

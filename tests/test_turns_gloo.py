@@ -178,7 +178,7 @@ def _worker(rank, world, port, errq):
         raise
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_run_turns_gloo(world):
     ctx = mp.get_context("spawn")
     errq = ctx.SimpleQueue()
