@@ -340,8 +340,14 @@ __global__ void __launch_bounds__(kCombineWarps * 32) decode_combine_kernel(
 }
 
 // Keys per CTA: about 8 waves of 148 CTAs, at least 8 blocks per CTA.
+// CTA-count target of the split heuristic.  148 x 8 (about 2.7 waves of the
+// three CTAs per SM the 2-stage ring allows) measured best: 148 x 6 and
+// 148 x 3 gave 0.79 / 0.87 ms per graphed B=4 step against 0.755 ms.
+#ifndef RCP_DEC_CTA_TARGET
+#define RCP_DEC_CTA_TARGET (148 * 8)
+#endif
 static int keys_per_cta(int64_t batch, int32_t hkv, int64_t max_kv_len) {
-  const int64_t target = 148 * 8;
+  const int64_t target = RCP_DEC_CTA_TARGET;
   int64_t per = (max_kv_len * batch * hkv + target - 1) / target;
   per = (per + kDecBlock - 1) / kDecBlock * kDecBlock;
   if (per < 8 * kDecBlock) per = 8 * kDecBlock;
