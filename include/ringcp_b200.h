@@ -114,6 +114,21 @@ int rcp_decode_attn(const void* q, const void* k, const void* v, int64_t kv_row_
                     int64_t max_kv_len, int32_t hq, int32_t hkv, int32_t head_dim, float scale,
                     float* o, float* lse, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Peer memory for the fused pass-Q All2All (Alg. 3's partial return,
+ * SPEC.md:249-257): instead of an All2All after the ring, each ring step's
+ * attention writes its partial O / LSE straight into the owning rank's
+ * receive buffer over NVLink.  rcp_ipc_alloc makes a device allocation of
+ * its own (cudaMalloc, so the exported handle covers exactly it) and returns
+ * its RCP_IPC_HANDLE_BYTES opaque handle, exchanged by the host transport;
+ * rcp_ipc_open maps a peer's allocation into the CURRENT device's address
+ * space (peer access enabled lazily; no extra CUDA context on the peer);
+ * rcp_ipc_close unmaps it and rcp_ipc_free releases an own allocation. */
+#define RCP_IPC_HANDLE_BYTES 64
+int rcp_ipc_alloc(size_t bytes, void** dev_ptr_out, void* handle_out);
+int rcp_ipc_free(void* dev_ptr);
+int rcp_ipc_open(const void* handle, void** dev_ptr_out);
+int rcp_ipc_close(void* dev_ptr);
+
 #ifdef __cplusplus
 }
 #endif

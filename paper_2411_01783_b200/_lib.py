@@ -32,6 +32,10 @@ _f32 = ctypes.c_float
 
 # name -> (restype, argtypes); mirrors include/ringcp_b200.h
 SIGNATURES = {
+    "rcp_ipc_alloc": (ctypes.c_int, [_size_t, ctypes.POINTER(_c_void_p), _c_void_p]),
+    "rcp_ipc_free": (ctypes.c_int, [_c_void_p]),
+    "rcp_ipc_open": (ctypes.c_int, [_c_void_p, ctypes.POINTER(_c_void_p)]),
+    "rcp_ipc_close": (ctypes.c_int, [_c_void_p]),
     "rcp_last_error": (ctypes.c_char_p, []),
     "rcp_version": (ctypes.c_char_p, []),
     "rcp_attn_workspace_bytes": (_size_t, [_i64, _i64]),

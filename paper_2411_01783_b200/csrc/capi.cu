@@ -323,3 +323,41 @@ int rcp_shard_gather(void* dst, const void* const* src_rows, const int64_t* new_
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ peer memory (CUDA IPC)
+extern "C" int rcp_ipc_alloc(size_t bytes, void** dev_ptr_out, void* handle_out) {
+  RCP_CHECK_ARG(bytes > 0 && dev_ptr_out != nullptr && handle_out != nullptr, "bad arguments");
+  static_assert(sizeof(cudaIpcMemHandle_t) == RCP_IPC_HANDLE_BYTES, "IPC handle size");
+  RCP_CUDA(cudaMalloc(dev_ptr_out, bytes));
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, *dev_ptr_out);
+  if (e != cudaSuccess) {
+    cudaFree(*dev_ptr_out);
+    *dev_ptr_out = nullptr;
+    set_error("cudaIpcGetMemHandle failed: %s", cudaGetErrorString(e));
+    return RCP_ERR_CUDA;
+  }
+  memcpy(handle_out, &h, sizeof(h));
+  return RCP_OK;
+}
+
+extern "C" int rcp_ipc_free(void* dev_ptr) {
+  RCP_CHECK_ARG(dev_ptr != nullptr, "null pointer");
+  RCP_CUDA(cudaFree(dev_ptr));
+  return RCP_OK;
+}
+
+extern "C" int rcp_ipc_open(const void* handle, void** dev_ptr_out) {
+  RCP_CHECK_ARG(handle != nullptr && dev_ptr_out != nullptr, "null pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  RCP_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return RCP_OK;
+}
+
+extern "C" int rcp_ipc_close(void* dev_ptr) {
+  RCP_CHECK_ARG(dev_ptr != nullptr, "null pointer");
+  RCP_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return RCP_OK;
+}
+

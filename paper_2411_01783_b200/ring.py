@@ -89,6 +89,69 @@ class StepTrace:
         return "\n".join(lines) + "\n"
 
 
+class _DevPtr:
+    """A raw device address where the C-ABI wrappers expect a tensor (only
+    ``data_ptr`` is used for parts, outputs and peer-mapped buffers)."""
+
+    def __init__(self, p: int):
+        self._p = int(p)
+
+    def data_ptr(self) -> int:
+        return self._p
+
+
+class PeerPartials:
+    """Receive buffers for pass-Q partials, one per rank, mapped on every peer.
+
+    Rank r's buffer holds N slots of (O [S, Hq, D] fp32, LSE [S, Hq] fp32),
+    slot s = the partial of r's queries against rank s's KV.  Allocated with
+    rcp_ipc_alloc and opened on every other rank with rcp_ipc_open (CUDA IPC
+    over NVLink), so rank s's attention kernel writes slot s of rank r's buffer
+    directly — the All2All of Alg. 3 becomes the kernels' own stores."""
+
+    def __init__(self, comm, S: int, H: int, D: int, device):
+        import ctypes
+
+        lib = _lib.load()
+        n, k = comm.world, comm.rank
+        self.S, self.H, self.D, self.n = S, H, D, n
+        self.o_slot = S * H * D * 4
+        self.l_slot = _align(S * H * 4)
+        total = n * (self.o_slot + self.l_slot)
+        own = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(64)
+        with torch.cuda.device(device):
+            _lib.check(lib.rcp_ipc_alloc(total, ctypes.byref(own), handle))
+            handles = comm.all_gather_bytes(handle.raw)
+            self.base = []
+            self._opened = []
+            for r in range(n):
+                if r == k:
+                    self.base.append(own.value)
+                    continue
+                p = ctypes.c_void_p()
+                _lib.check(lib.rcp_ipc_open(handles[r], ctypes.byref(p)))
+                self.base.append(p.value)
+                self._opened.append(p.value)
+        self._own = own.value
+        self.device = device
+
+    def o(self, owner: int, src: int) -> _DevPtr:
+        return _DevPtr(self.base[owner] + src * self.o_slot)
+
+    def lse(self, owner: int, src: int) -> _DevPtr:
+        return _DevPtr(self.base[owner] + self.n * self.o_slot + src * self.l_slot)
+
+    def close(self) -> None:
+        lib = _lib.load()
+        with torch.cuda.device(self.device):
+            for p in self._opened:
+                lib.rcp_ipc_close(_DevPtr(p).data_ptr())
+            if self._own:
+                lib.rcp_ipc_free(self._own)
+        self._opened, self._own = [], 0
+
+
 @dataclass
 class HostStage:
     """Inputs of one host-buffer prefill staged on the device by
@@ -245,6 +308,20 @@ class TorchRingComm:
     def _g(self, r: int) -> int:
         return r if self.group is None else self.dist.get_global_rank(self.group, r)
 
+    def stream_barrier(self, device) -> None:
+        """All ranks' work queued so far on their current streams completes
+        before work queued after this on any rank (a one-element NCCL
+        all-reduce on the stream; no host synchronisation)."""
+        t = getattr(self, "_bar_t", None)
+        if t is None or t.device != device:
+            t = self._bar_t = torch.zeros(1, dtype=torch.int32, device=device)
+        self.dist.all_reduce(t, group=self.group)
+
+    def all_gather_bytes(self, data: bytes) -> list:
+        out = [None] * self.world
+        self.dist.all_gather_object(out, data, group=self.group)
+        return out
+
     def exchange(self, send: torch.Tensor, recv: torch.Tensor):
         d = self.dist
         ops = [d.P2POp(d.isend, send, self._g(self.topo.next(self.rank)), self.group),
@@ -334,6 +411,9 @@ class RingAttention:
         # (each step re-reads this rank's own block) — same kernels and shapes,
         # used to compute the exposed-communication fraction.
         self.no_comm = False
+        # pass-Q partials written straight into the owners' peer-mapped
+        # receive slots instead of an All2All (NCCL ranks on one node only)
+        self.fused_a2a = False
 
     def _buf(self, key, nbytes, device):
         b = self._bufs.get(key)
@@ -522,13 +602,49 @@ class RingAttention:
         return PartialAttention(blk, lse)
 
     # -------------------------------------------------------------- Alg. 3
+    def _peer_partials(self, S, H, D, dev) -> PeerPartials:
+        pp = self._bufs.get(("peer", S, H, D))
+        if pp is None:
+            pp = PeerPartials(self.comm, S, H, D, dev)
+            self._bufs[("peer", S, H, D)] = pp
+        return pp
+
     def pass_q(self, q_lay: QLayout, q_msg: torch.Tensor, kk, vv, kp, ks, cfg: GqaConfig,
                out: torch.Tensor, lse: torch.Tensor, dtype=torch.bfloat16):
         """Ring pass-Q over prepared buffers, then All2All of the partials and the
-        merge in pass-KV arrival order."""
+        merge in pass-KV arrival order.  With ``self.fused_a2a`` (NCCL ranks on
+        one NVLink domain) each step's attention writes its partial straight
+        into the owner's peer-mapped receive slot instead (PeerPartials), and
+        the All2All reduces to a stream-ordered barrier; the partials and the
+        merge order are the same, so the result is bitwise identical."""
         n, k = self.comm.world, self.comm.rank
         dev = q_msg.device
         S, H, D = q_lay.tokens, cfg.n_query_heads, cfg.head_dim
+        if self.fused_a2a and n > 1:
+            pp = self._peer_partials(S, H, D, dev)
+            self.comm.stream_barrier(dev)  # owners finished reading their slots (previous call)
+            bufs = [self._buf(("q", 0), q_lay.nbytes, dev), self._buf(("q", 1), q_lay.nbytes, dev)]
+            cur = q_msg
+            for step in range(n):
+                src = (k - step) % n
+                works = None
+                nxt = None
+                if step < n - 1:
+                    nxt = bufs[step % 2]
+                    works = self.comm.exchange(cur, nxt)
+                    if self.trace is not None:
+                        self.trace.add(step, k, "Q", q_lay.nbytes)
+                qq, qp, qs = q_lay.views(cur, dtype)
+                # the partial of src's queries against this rank's KV goes to src's slot k
+                self.attend(qq, qp, qs, kk, vv, kp, ks, cfg, pp.o(src, k), pp.lse(src, k), _lib.MODE_OVERWRITE)
+                self.comm.wait(works)
+                cur = nxt
+            self.comm.stream_barrier(dev)  # every partial for this rank has landed
+            if self.trace is not None:
+                self.trace.add(n - 1, k, "A2A", 0)
+            order = [(k - j) % n for j in range(n)]
+            self.merge([pp.o(k, s) for s in order], [pp.lse(k, s) for s in order], out, lse)
+            return out, lse
         send_o = [torch.empty((S, H, D), dtype=torch.float32, device=dev) for _ in range(n)]
         send_l = [torch.empty((S, H), dtype=torch.float32, device=dev) for _ in range(n)]
         bufs = [self._buf(("q", 0), q_lay.nbytes, dev), self._buf(("q", 1), q_lay.nbytes, dev)]

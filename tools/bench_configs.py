@@ -114,6 +114,23 @@ def run_partial(args, rank, world):
             fn = (lambda: ring.pass_kv_prefill(plan, cache, qb, kb, vb, cfg)) if proto == "pass_kv" else \
                  (lambda: ring.pass_q_prefill(plan, cache, qb, kb, vb, cfg))
             res[proto] = timed(fn, reset, args.steps, args.warmup, world)
+        fused = None
+        if args.fused and world > 1:
+            # pass-Q with the partials written straight into the owners' peer
+            # slots (no All2All): must equal the All2All version bit for bit
+            reset()
+            ref = ring.pass_q_prefill(plan, cache, qb, kb, vb, cfg)
+            ring.fused_a2a = True
+            reset()
+            got = ring.pass_q_prefill(plan, cache, qb, kb, vb, cfg)
+            torch.cuda.synchronize()
+            same = torch.tensor([int(torch.equal(ref.output.data, got.output.data) and torch.equal(ref.lse, got.lse))],
+                                device="cuda")
+            dist.all_reduce(same, op=dist.ReduceOp.MIN)
+            assert int(same.item()) == 1, "fused pass-Q differs from the All2All version"
+            fused = timed(lambda: ring.pass_q_prefill(plan, cache, qb, kb, vb, cfg), reset, args.steps,
+                          args.warmup, world)
+            ring.fused_a2a = False
         shape = pm.PrefillShape(T, P)
         pick = pm.choose_strategy(shape, m)
         pick_ref = pm.choose_strategy(shape, m, refined=True)
@@ -123,6 +140,7 @@ def run_partial(args, rank, world):
             print(json.dumps({
                 "config": "cfg4-partial-prefill", "cp": world, "n_q_heads": hq, "n_kv_heads": hkv,
                 "P": P, "T": T, "miss": T / total, "pass_kv_ms": res["pass_kv"], "pass_q_ms": res["pass_q"],
+                "pass_q_fused_a2a_ms": fused,
                 "winner": best, "heuristic": pick, "heuristic_refined": pick_ref,
                 "tflops_per_gpu_best": flops / (res[best] * 1e-3) / 1e12 / world}), flush=True)
         del cache
@@ -197,6 +215,8 @@ def main():
     ap.add_argument("--batch", type=int, nargs="*", default=[1, 2, 4, 8, 16, 32])
     ap.add_argument("--gather", action="store_true", help="decode: all-gather Q instead of the Q ring")
     ap.add_argument("--graph", action="store_true", help="decode: replay the step from a CUDA graph")
+    ap.add_argument("--fused", action="store_true",
+                    help="partial: also time pass-Q with peer-memory partials (no All2All), checked bitwise")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     args = ap.parse_args()
