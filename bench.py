@@ -17,6 +17,12 @@ work fixed: strong scaling).  Inputs (1 GB Q, 268 MB K/V at CP1) exceed the
 Prints ONE JSON line on rank 0 (metric, value = whole-job TFLOP/s, roofline of
 the attention kernel, CPU baseline of the oracle port, e2e through the public
 API with host buffers, clocks sampled during the timed region).
+
+e2e: K steps of RingAttention.pass_kv_prefill_host from pinned host buffers,
+run as a serving loop — each step's inputs are staged H2D one step ahead on a
+copy stream (stage_host_inputs) and each query range's final O / LSE goes D2H
+as soon as it is final; every step's H2D and D2H are inside the timed region,
+which ends after the D2H stream is joined (join_host_copies).
 """
 
 from __future__ import annotations
