@@ -409,8 +409,12 @@ class RingAttention:
         self.trace: StepTrace | None = None
         # Measurement hook: True replaces every ring transfer by a local no-op
         # (each step re-reads this rank's own block) — same kernels and shapes,
-        # used to compute the exposed-communication fraction.
+        # used to compute the exposed-communication fraction;
+        # "pregathered" runs each step on the very block the ring would
+        # deliver, all-gathered once beforehand (pregather_kv), so the work of
+        # every step is identical to the ring's and only the transfers go.
         self.no_comm = False
+        self._pregathered = None
         # pass-Q partials written straight into the owners' peer-mapped
         # receive slots instead of an All2All (NCCL ranks on one node only)
         self.fused_a2a = False
@@ -438,10 +442,13 @@ class RingAttention:
         splits = q_splits or [(0, q.shape[0])]
         bufs = [self._buf(("kv", 0), kv_lay.nbytes, dev), self._buf(("kv", 1), kv_lay.nbytes, dev)]
         cur = kv_msg
+        pre = self._pregathered if self.no_comm == "pregathered" else None
         for step in range(n):
             works = None
             nxt = None
-            if step < n - 1 and self.no_comm:
+            if pre is not None:  # the block the ring would deliver, gathered beforehand
+                cur = pre[(k - step) % n][: kv_lay.nbytes]
+            elif step < n - 1 and self.no_comm:
                 nxt = cur
             elif step < n - 1:
                 nxt = bufs[step % 2]
@@ -459,6 +466,14 @@ class RingAttention:
             self.comm.wait(works)
             cur = nxt
         return out, lse
+
+    def pregather_kv(self) -> None:
+        """All-gather every rank's current local KV message (from the last
+        prefill) for the "pregathered" measurement mode."""
+        local = self._bufs[("kv", "local")]
+        allb = torch.empty((self.comm.world, local.numel()), dtype=torch.uint8, device=local.device)
+        self.comm.wait(self.comm.all_gather(local, allb.view(-1)))
+        self._pregathered = [allb[r] for r in range(self.comm.world)]
 
     def _side_stream(self, key):
         s = self._bufs.get(("stream", key))
