@@ -125,22 +125,38 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------- CPU arms
+_KV = {}
+
+
+def _oracle_kv(T, hkv):
+    """Synthetic K/V of the sample, made once per worker process and reused by
+    every step (the GPU arm likewise builds its inputs before timing)."""
+    if (T, hkv) not in _KV:
+        _KV.clear()
+        rng = np.random.default_rng(12345)
+        _KV[(T, hkv)] = (rng.standard_normal((T, hkv, D)).astype(np.float32),
+                         rng.standard_normal((T, hkv, D)).astype(np.float32))
+    return _KV[(T, hkv)]
+
+
 def _oracle_worker(args):
     """Bounded sample of the workload for the oracle port: `rows` query rows
     spread over the second half of the sequence, each attending (causally) to
-    all T keys, evaluated one query head at a time so the oracle's fp64
-    temporaries stay ~0.4 GB per worker.  Returns (seconds, admitted pairs)."""
-    T, hq, hkv, rows, seed = args
+    all T keys, for query heads 0, stride, 2·stride, ... one head per call (the
+    oracle's fp64 temporaries stay ~0.4 GB per worker).  Returns (seconds,
+    admitted (query, key, head) triples)."""
+    T, hq, hkv, rows, seed = args[:5]
+    head_stride = args[5] if len(args) > 5 else 1
     from oracle import ringcp_oracle as orc
 
     rng = np.random.default_rng(seed)
     q_pos = np.linspace(T // 2, T - 1, rows).astype(np.int64)
     qd = rng.standard_normal((rows, hq, D)).astype(np.float32)
-    kd = rng.standard_normal((T, hkv, D)).astype(np.float32)
-    vd = rng.standard_normal((T, hkv, D)).astype(np.float32)
+    kd, vd = _oracle_kv(T, hkv)
     kpos = np.arange(T)
     dt = 0.0
-    for h in range(hq):
+    heads = range(0, hq, head_stride)
+    for h in heads:
         g = (h * hkv) // hq  # GqaConfig.query_to_kv_head (attention.py:64-66)
         q = orc.blk_from_tokens(qd[:, h:h + 1], q_pos)
         k = orc.blk_from_tokens(kd[:, g:g + 1], kpos)
@@ -148,7 +164,7 @@ def _oracle_worker(args):
         t0 = time.perf_counter()
         orc.gqa(q, k, v, 1, 1.0 / np.sqrt(D))
         dt += time.perf_counter() - t0
-    return dt, int((q_pos + 1).sum())
+    return dt, int((q_pos + 1).sum()) * len(heads)  # admitted (query, key, head) triples
 
 
 def _worker_budget(cores: int) -> int:
@@ -163,8 +179,8 @@ def _worker_budget(cores: int) -> int:
 
 def cpu_baseline_port(T, hq, hkv, rows=16):
     """Oracle port (the reference's numpy algorithm), single process = 1 core."""
-    dt, pairs = _oracle_worker((T, hq, hkv, rows, 7))
-    flops = 4.0 * D * hq * pairs
+    dt, triples = _oracle_worker((T, hq, hkv, rows, 7))
+    flops = 4.0 * D * triples
     return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": 1, "kind": "port",
             "sample": f"{rows} query rows x {T} keys x {hq}/{hkv} heads (positions {T // 2}..{T - 1}), "
                       f"oracle gqa {dt:.2f} s"}
@@ -180,8 +196,12 @@ def run_reference(args, cfg, rank, world):
     T, hq, hkv = cfg["T"], cfg["hq"], cfg["hkv"]
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     cores = _worker_budget(cores)
-    rows_per = 2
-    jobs = [(T, hq, hkv, rows_per, 100 + i) for i in range(cores)]
+    # per step: every process evaluates rows_per query rows against all T keys
+    # for every query head (short runs) or one query head per KV group (long
+    # runs), keeping the whole arm within a few minutes
+    short = args.steps + args.warmup <= 10
+    rows_per, head_stride = (2, 1) if short else (1, hq // hkv)
+    jobs = [(T, hq, hkv, rows_per, 100 + i, head_stride) for i in range(cores)]
     ctx = mp.get_context("fork")
     vals = []
     with ctx.Pool(cores) as pool:
@@ -189,9 +209,9 @@ def run_reference(args, cfg, rank, world):
             t0 = time.perf_counter()
             res = pool.map(_oracle_worker, jobs)
             dt = time.perf_counter() - t0
-            pairs = sum(r[1] for r in res)
+            triples = sum(r[1] for r in res)
             if it >= args.warmup:
-                vals.append(4.0 * D * hq * pairs / dt / 1e12)
+                vals.append(4.0 * D * triples / dt / 1e12)
     value = statistics.median(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
@@ -201,7 +221,8 @@ def run_reference(args, cfg, rank, world):
         "config": {"workload": cfg["workload"], "seq_len": T, "n_q_heads": hq, "n_kv_heads": hkv,
                    "head_dim": D, "cp": world},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                         "sample": f"{cores} processes x {rows_per} query rows x {T} keys per step"},
+                         "sample": f"{cores} processes x {rows_per} query rows x {T} keys x "
+                                   f"{len(range(0, hq, head_stride))} query heads per step"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -414,7 +435,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="8b", choices=sorted(CONFIGS))
