@@ -9,7 +9,7 @@ ctypes / allocator work per step at B = 1 against ~250 us of GPU time,
 DESIGN.md), so ``GraphedDecode`` captures those launches once and replays
 them; per step the host only does the cache bookkeeping and ONE pinned
 host->device copy of the step's metadata (arena rows to append to,
-positions, per-query KV segments).
+per-query KV segments, positions and sequence ids of the appends).
 
 Static shapes: the batch, its slot assignment pattern and the arena must not
 change while a graph is live.  ``GraphedDecode`` reserves room for
@@ -75,8 +75,8 @@ class GraphedDecode:
         self.q_in = torch.zeros((S, H, D), dtype=torch.bfloat16, device=dev)
         self.k_in = torch.zeros((S, Hkv, D), dtype=cache.dtype, device=dev)
         self.v_in = torch.zeros_like(self.k_in)
-        self.meta = torch.zeros(S + 2 * R, dtype=torch.int64, device=dev)   # rows | starts | lens
-        self.meta32 = torch.zeros(2 * S, dtype=torch.int32, device=dev)     # pos | seq of appends
+        # rows | starts | lens | pos | seq (one host->device copy per step)
+        self.meta = torch.zeros(S + 2 * R + 2 * S, dtype=torch.int64, device=dev)
         self.q_all = torch.zeros((R, H, D), dtype=torch.bfloat16, device=dev)
         self.part_o = torch.empty((R, H, D), dtype=torch.float32, device=dev)
         self.part_l = torch.empty((R, H), dtype=torch.float32, device=dev)
@@ -96,10 +96,11 @@ class GraphedDecode:
         rows = self.meta[:S]
         c.k.index_copy_(0, rows, self.k_in)
         c.v.index_copy_(0, rows, self.v_in)
-        c.pos.index_copy_(0, rows, self.meta32[:S])
-        c.seq.index_copy_(0, rows, self.meta32[S:])
         R = self.n * S
-        starts, lens = self.meta[S:S + R], self.meta[S + R:]
+        meta32 = self.meta[S + 2 * R:].to(torch.int32)  # pos | seq of the appends
+        c.pos.index_copy_(0, rows, meta32[:S])
+        c.seq.index_copy_(0, rows, meta32[S:])
+        starts, lens = self.meta[S:S + R], self.meta[S + R:S + 2 * R]
         if self.n == 1:
             _cuda_decode(self.q_in, c.k, c.v, starts, lens, self.max_len, self.cfg, self.out, self.lse, self.ws)
             return
@@ -146,7 +147,7 @@ class GraphedDecode:
         for src in range(n):
             for j, (sid, _b) in enumerate(plan.assignments[src]):
                 starts[src * S + j], lens[src * S + j] = c.segment(sid)
-        return np.concatenate([rows, starts, lens]), np.concatenate([pos32, seq32]).astype(np.int32)
+        return np.concatenate([rows, starts, lens, pos32, seq32])
 
     def step(self, q_tok: torch.Tensor, k_tok: torch.Tensor, v_tok: torch.Tensor, positions):
         if self.steps_left <= 0:
@@ -158,9 +159,8 @@ class GraphedDecode:
             self.q_in[:m].copy_(q_tok[:m])
             self.k_in[:m].copy_(k_tok[:m])
             self.v_in[:m].copy_(v_tok[:m])
-        meta, meta32 = self._host_meta(mine, positions)
+        meta = self._host_meta(mine, positions)
         self.meta.copy_(_lib.h2d(meta, self.cache.device), non_blocking=True)
-        self.meta32.copy_(_lib.h2d(meta32, self.cache.device), non_blocking=True)
         ptrs = (self.cache.k.data_ptr(), self.cache.v.data_ptr(), self.cache.pos.data_ptr(),
                 self.cache.seq.data_ptr())
         if self.graph is None or ptrs != self._arena_ptr:
