@@ -23,7 +23,6 @@ so pass-KV and pass-Q are bit-identical.
 
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass, field
 
 import numpy as np

@@ -28,7 +28,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import perf_model as pm
-from .attention import GqaConfig, PartialAttention
+from .attention import GqaConfig
 from .kv_cache import RankKvCache
 from .ring import RingAttention, StepTrace
 from .sharding import (SequenceSpec, materialize_rank_block, plan_decode, plan_full_prefill,

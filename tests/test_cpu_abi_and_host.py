@@ -3,7 +3,6 @@ declares; host-side plan logic matches the reference's golden plans; message
 layouts and the ring topology.  No kernel is launched here."""
 
 import ctypes
-import math
 import os
 import re
 

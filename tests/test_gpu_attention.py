@@ -1,7 +1,6 @@
 """GPU parity of gqa_attention / merge_attention (C-ABI kernels) vs the oracle
 and the golden vectors produced by the real reference."""
 
-import math
 
 import numpy as np
 import pytest

@@ -167,7 +167,6 @@ def test_partial_prefill_and_decode_vs_oracle(rc):
     qb = [materialize_rank_block(plan, r, [dev(x) for x in q]) for r in range(n)]
     kb = [materialize_rank_block(plan, r, [dev(x) for x in k]) for r in range(n)]
     vb = [materialize_rank_block(plan, r, [dev(x) for x in v]) for r in range(n)]
-    import copy
     caches_g2 = caches_g  # pass-Q needs its own caches: rebuild by replay is costly; compare pass-KV here
     got = ring_pass_kv_prefill(plan, caches_g2, qb, kb, vb, cfg)
     oseqs = [orc.Seq(s, P, t) for s, P, t in zip(batch, lens, T1)]

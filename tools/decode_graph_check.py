@@ -12,7 +12,6 @@ import os
 import statistics
 import sys
 
-import numpy as np
 import torch
 import torch.distributed as dist
 

@@ -22,7 +22,7 @@ from paper_2411_01783_b200.kv_cache import RankKvCache  # noqa: E402
 from paper_2411_01783_b200.ring import (RingAttention, TorchRingComm, ring_pass_kv_prefill,  # noqa: E402
                                         ring_pass_q_prefill)
 from paper_2411_01783_b200.sharding import (SequenceSpec, materialize_rank_block,  # noqa: E402
-                                            plan_full_prefill, plan_partial_prefill)
+                                            plan_full_prefill)
 
 
 def main():

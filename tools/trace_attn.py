@@ -21,7 +21,6 @@ _lib.LIB_PATH = os.path.join(ROOT, "paper_2411_01783_b200", os.environ.get("RCP_
 lib = _lib.load()
 lib.rcp_debug_set_trace.argtypes = [ctypes.c_void_p]
 
-import paper_2411_01783_b200 as rc  # noqa: E402
 from paper_2411_01783_b200.attention import attend_into  # noqa: E402
 
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
