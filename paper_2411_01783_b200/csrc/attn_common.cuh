@@ -127,6 +127,20 @@ __device__ __forceinline__ float ex2_poly(float x) {
   // (bits(t) << 23) == round(x) << 23 modulo 2^32 because 0x4B400000 << 23 == 0
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
+// ex2_poly on a pair with the rounding split and Horner steps on FADD2 / FFMA2
+// (same IEEE operations, so bitwise equal to two ex2_poly calls).
+__device__ __forceinline__ float2 ex2_poly_x2(float a, float b) {
+  const uint64_t x2 = f2(fmaxf(a, -126.0f), fmaxf(b, -126.0f));
+  const uint64_t t = fadd2(x2, f2(12582912.0f, 12582912.0f));
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x2), "l"(fadd2(t, f2(-12582912.0f, -12582912.0f))));
+  uint64_t pp = ffma2(f2(0.05500893f, 0.05500893f), r, f2(0.24221097f, 0.24221097f));
+  pp = ffma2(pp, r, f2(0.69328290f, 0.69328290f));
+  pp = ffma2(pp, r, f2(1.0f, 1.0f));
+  const float2 pf = unf2(pp), tf = unf2(t);
+  return make_float2(__int_as_float(__float_as_int(pf.x) + (__float_as_int(tf.x) << 23)),
+                     __int_as_float(__float_as_int(pf.y) + (__float_as_int(tf.y) << 23)));
+}
 
 
 // ---- CTA-pair (cta_group::2) primitives used by the v5 / v8 variants

@@ -302,8 +302,11 @@ __global__ void __launch_bounds__(kThreads6, 1) attn_fwd_v6_kernel(const __grid_
               const float2 x = unf2(ffma2(f2(s[2 * ip], s[2 * ip + 1]), sl2x2, negm2));
               float p0, p1;
               if ((ip & 7) < kPolyPairsPer8) {
-                p0 = ex2_poly(x.x);
-                p1 = ex2_poly(x.y);
+                {
+                  const float2 pp_ = ex2_poly_x2(x.x, x.y);
+                  p0 = pp_.x;
+                  p1 = pp_.y;
+                }
               } else {
                 p0 = ex2_approx(x.x);
                 p1 = ex2_approx(x.y);
@@ -663,8 +666,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_v7_kernel(const __grid_c
               const float2 x = unf2(ffma2(f2(s[2 * ip], s[2 * ip + 1]), sl2x2, negm2));
               float p0, p1;
               if ((ip & 7) < kPolyPairsPer8) {
-                p0 = ex2_poly(x.x);
-                p1 = ex2_poly(x.y);
+                {
+                  const float2 pp_ = ex2_poly_x2(x.x, x.y);
+                  p0 = pp_.x;
+                  p1 = pp_.y;
+                }
               } else {
                 p0 = ex2_approx(x.x);
                 p1 = ex2_approx(x.y);
@@ -1049,8 +1055,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             const float2 x = unf2(ffma2(f2(s[2 * i], s[2 * i + 1]), sl2x2, negm2));
             float p0, p1;
             if ((i & 7) < kPolyPairsPer8) {
-              p0 = ex2_poly(x.x);
-              p1 = ex2_poly(x.y);
+              {
+                const float2 pp_ = ex2_poly_x2(x.x, x.y);
+                p0 = pp_.x;
+                p1 = pp_.y;
+              }
             } else {
               p0 = ex2_approx(x.x);
               p1 = ex2_approx(x.y);
@@ -1407,8 +1416,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const float2 xx = unf2(ffma2(f2(s[2 * ip], s[2 * ip + 1]), sl2x2, negm2));
               float p0, p1;
               if ((ip & 7) < kPolyPairsPer8) {
-                p0 = ex2_poly(xx.x);
-                p1 = ex2_poly(xx.y);
+                {
+                  const float2 pp_ = ex2_poly_x2(xx.x, xx.y);
+                  p0 = pp_.x;
+                  p1 = pp_.y;
+                }
               } else {
                 p0 = ex2_approx(xx.x);
                 p1 = ex2_approx(xx.y);
