@@ -6,7 +6,10 @@ pass-KV ring), each launch timed alone with CUDA events (median of 5) on
 admitted-pair FLOPs.  Separates kernel efficiency at small launch shapes from
 the host/ring overheads cp_shape_efficiency.py includes.
 
-  python tools/cp_shape_kernel.py [T]
+  python tools/cp_shape_kernel.py [T] [merge]
+
+With "merge" every launch folds into a running (O, LSE) (RCP_MODE_MERGE, what
+ring steps after the first do).
 """
 import os
 import statistics
@@ -23,6 +26,7 @@ from paper_2411_01783_b200.attention import admitted_pair_count, attend_into  # 
 from paper_2411_01783_b200.sharding import SequenceSpec, materialize_rank_block, plan_full_prefill  # noqa: E402
 
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
+MODE = _lib.MODE_MERGE if "merge" in sys.argv[2:] else _lib.MODE_OVERWRITE
 hq, hkv, D = 32, 8, 128
 cfg = rc.GqaConfig(hq, hkv, D)
 g = torch.Generator(device="cuda").manual_seed(0)
@@ -39,8 +43,8 @@ for n in (1, 2, 4, 8):
         vb = materialize_rank_block(plan, src, [v])
         kk, vv = kb.valid_only(), vb.valid_only()
         flops = 4.0 * D * hq * admitted_pair_count(qb, kk)
-        out = torch.empty(qb.n_tokens, hq, D, device="cuda")
-        lse = torch.empty(qb.n_tokens, hq, device="cuda")
+        out = torch.zeros(qb.n_tokens, hq, D, device="cuda")
+        lse = torch.zeros(qb.n_tokens, hq, device="cuda")
         ws = torch.empty(max(_lib.load().rcp_attn_workspace_bytes(qb.n_tokens, kk.n_tokens), 32),
                          dtype=torch.uint8, device="cuda")
         ts = []
@@ -49,7 +53,7 @@ for n in (1, 2, 4, 8):
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
             attend_into(qb.data, qb.meta32("q"), kk.data, vv.data, kk.meta32("k"), hq, hkv, cfg.scale,
-                        out, lse, _lib.MODE_OVERWRITE, workspace=ws)
+                        out, lse, MODE, workspace=ws)
             e.record()
             torch.cuda.synchronize()
             ts.append(s.elapsed_time(e))
