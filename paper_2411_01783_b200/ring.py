@@ -113,10 +113,9 @@ class PeerPartials:
 
         lib = _lib.load()
         n, k = comm.world, comm.rank
-        self.S, self.H, self.D, self.n = S, H, D, n
-        self.o_slot = S * H * D * 4
-        self.l_slot = _align(S * H * 4)
-        total = n * (self.o_slot + self.l_slot)
+        self.n = n
+        self.set_shape(S, H, D)
+        total = self.capacity = self.bytes_for(n, S, H, D)
         own = ctypes.c_void_p()
         handle = ctypes.create_string_buffer(64)
         with torch.cuda.device(device):
@@ -135,20 +134,43 @@ class PeerPartials:
         self._own = own.value
         self.device = device
 
+    @staticmethod
+    def bytes_for(n: int, S: int, H: int, D: int) -> int:
+        return n * (S * H * D * 4 + _align(S * H * 4))
+
+    def fits(self, S: int, H: int, D: int) -> bool:
+        return self.bytes_for(self.n, S, H, D) <= self.capacity
+
+    def set_shape(self, S: int, H: int, D: int) -> None:
+        """Re-slot the same allocation for another (S, H, D); every rank does
+        this for the same call (pass-Q messages have equal sizes), and the
+        caller's stream barrier orders it after the previous call's writes."""
+        self.S, self.H, self.D = S, H, D
+        self.o_slot = S * H * D * 4
+        self.l_slot = _align(S * H * 4)
+
     def o(self, owner: int, src: int) -> _DevPtr:
         return _DevPtr(self.base[owner] + src * self.o_slot)
 
     def lse(self, owner: int, src: int) -> _DevPtr:
         return _DevPtr(self.base[owner] + self.n * self.o_slot + src * self.l_slot)
 
-    def close(self) -> None:
+    def close(self, comm=None) -> None:
+        """Unmap the peers' buffers and free this rank's.  With ``comm`` (all
+        ranks call together) every rank has finished its kernels and unmapped
+        before any owner frees."""
         lib = _lib.load()
         with torch.cuda.device(self.device):
+            torch.cuda.synchronize()
             for p in self._opened:
                 lib.rcp_ipc_close(_DevPtr(p).data_ptr())
+            self._opened = []
+            if comm is not None and comm.world > 1:
+                comm.stream_barrier(self.device)
+                torch.cuda.synchronize()
             if self._own:
                 lib.rcp_ipc_free(self._own)
-        self._opened, self._own = [], 0
+        self._own = 0
 
 
 @dataclass
@@ -617,11 +639,24 @@ class RingAttention:
 
     # -------------------------------------------------------------- Alg. 3
     def _peer_partials(self, S, H, D, dev) -> PeerPartials:
-        pp = self._bufs.get(("peer", S, H, D))
-        if pp is None:
-            pp = PeerPartials(self.comm, S, H, D, dev)
-            self._bufs[("peer", S, H, D)] = pp
+        pp = self._bufs.get("peer")
+        if pp is not None and pp.device == dev and pp.fits(S, H, D):
+            pp.set_shape(S, H, D)
+            return pp
+        if pp is not None:  # grow: collective, every rank sees the same sizes
+            pp.close(self.comm)
+        pp = PeerPartials(self.comm, S, H, D, dev)
+        self._bufs["peer"] = pp
         return pp
+
+    def close(self) -> None:
+        """Release the ring's buffers; with ``fused_a2a`` this unmaps and frees
+        the peer-mapped partial buffers, so every rank must call it."""
+        pp = self._bufs.pop("peer", None)
+        if pp is not None:
+            pp.close(self.comm)
+        self._bufs.clear()
+        self._pregathered = None
 
     def pass_q(self, q_lay: QLayout, q_msg: torch.Tensor, kk, vv, kp, ks, cfg: GqaConfig,
                out: torch.Tensor, lse: torch.Tensor, dtype=torch.bfloat16):
