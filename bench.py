@@ -373,10 +373,9 @@ def run_ours(args, cfg, rank, world, local_rank):
             st = stage()
             for i in range(n):
                 cache.reset()
-                nxt = stage() if i + 1 < n else None
                 ring.pass_kv_prefill_host(plan, cache, [host["q"]], [host["k"]], [host["v"]], gcfg, out_host,
                                           lse_host, staged=st, join=False)
-                st = nxt
+                st = stage() if i + 1 < n else None  # next request's H2D runs under this one
             ring.join_host_copies()
 
         e2e_steps(2)

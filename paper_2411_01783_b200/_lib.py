@@ -120,18 +120,121 @@ def i64_array(vals):
     return (_i64 * len(vals))(*[int(v) for v in vals])
 
 
-def h2d(arr, device):
-    """Host array -> device tensor without a host/device sync: staged through
-    pinned memory (torch's caching host allocator keeps the staging block alive
-    until the copy has run) and copied with non_blocking=True.  A pageable
-    source would make the copy wait for all earlier work on the stream."""
+class _PinnedRing:
+    """One persistent page-locked staging arena for the small host->device
+    uploads of the hot path (metadata, index maps).  Allocating page-locked
+    memory (or device memory) between stream commands implicitly synchronises
+    the device, so a per-call pinned block — which torch's caching host
+    allocator cannot recycle while the host runs ahead of the GPU — stalls
+    the copy/compute overlap.  Regions are handed out circularly; each is
+    reused only after the event recorded behind its copy has completed (a host
+    wait only if the host is a whole arena ahead of the device)."""
+
+    def __init__(self, nbytes: int):
+        import collections
+
+        import torch
+
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        self.cap = nbytes
+        self.head = 0
+        self.live = collections.deque()  # (start, end, event), allocation order
+
+    def take(self, n: int):
+        n = (n + 255) // 256 * 256
+        if self.head + n > self.cap:
+            self.head = 0
+        a, b = self.head, self.head + n
+        while self.live and self.live[0][2].query():  # retire completed copies
+            self.live.popleft()
+        if any(s < b and a < e for s, e, _ in self.live):
+            keep = type(self.live)()
+            for s, e, ev in self.live:
+                if s < b and a < e:
+                    ev.synchronize()  # host a whole arena ahead: wait for that copy
+                else:
+                    keep.append((s, e, ev))
+            self.live = keep
+        self.head = b
+        return a, b
+
+    def commit(self, a: int, b: int) -> None:
+        import torch
+
+        ev = torch.cuda.Event()
+        ev.record()
+        self.live.append((a, b, ev))
+
+
+def _torch_dtype(arr):
     import numpy as np
     import torch
 
+    return torch.from_numpy(np.zeros(0, dtype=np.asarray(arr).dtype)).dtype
+
+
+_RING = None
+_RING_BYTES = 64 << 20
+_RING_MAX = 8 << 20
+
+
+_META_STREAMS = {}
+
+
+def _meta_stream(device):
+    import torch
+
+    key = torch.device(device).index
+    s = _META_STREAMS.get(key)
+    if s is None:
+        s = _META_STREAMS[key] = torch.cuda.Stream(device=device)
+    return s
+
+
+def h2d(arr, device, out=None):
+    """Host array -> device tensor (or into ``out``) without a host/device
+    sync: staged through the persistent pinned ring (_PinnedRing) and copied
+    with non_blocking=True.  Arrays above 8 MB get a dedicated pinned block
+    instead.  A pageable source would make the copy wait for all earlier work
+    on the stream.
+
+    Without ``out`` the copy runs on a dedicated metadata stream that depends
+    on nothing, and the current stream waits for it: copy engines serve
+    host->device copies in submission order, so a small copy ordered behind
+    the compute stream's earlier work would otherwise queue behind any large
+    transfer submitted meanwhile (e.g. the next request's staged inputs).
+    With ``out`` (the destination may still be in use) the copy is ordered on
+    the current stream."""
+    global _RING
+    import numpy as np
+    import torch
+
+    if out is None and torch.device(device).type == "cuda" and not torch.cuda.is_current_stream_capturing():
+        cur = torch.cuda.current_stream(device)
+        ms = _meta_stream(device)
+        with torch.cuda.stream(ms):
+            d = h2d(arr, device, out=torch.empty(np.shape(arr), dtype=_torch_dtype(arr), device=device))
+            ev = torch.cuda.Event()
+            ev.record(ms)
+        cur.wait_event(ev)
+        d.record_stream(cur)
+        return d
+
     t = torch.from_numpy(np.ascontiguousarray(arr))
     if device is None or torch.device(device).type != "cuda":
-        return t
-    staged = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-    staged.copy_(t)
-    return staged.to(device, non_blocking=True)
-
+        return t if out is None else out.copy_(t)
+    nbytes = t.numel() * t.element_size()
+    if nbytes == 0:
+        return torch.empty(t.shape, dtype=t.dtype, device=device) if out is None else out
+    if nbytes > _RING_MAX:
+        staged = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        staged.copy_(t)
+        return staged.to(device, non_blocking=True) if out is None else out.copy_(staged, non_blocking=True)
+    if _RING is None:
+        _RING = _PinnedRing(_RING_BYTES)
+    a, b = _RING.take(nbytes)
+    pv = _RING.buf[a:a + nbytes].view(t.dtype).view(t.shape)
+    pv.copy_(t)
+    d = pv.to(device, non_blocking=True) if out is None else out.copy_(pv, non_blocking=True)
+    _RING.commit(a, b)
+    return d

@@ -139,10 +139,11 @@ class RankKvCache:
         return self._append_rows(seq_id, k_block.data[idx], v_block.data[idx], pos_host)
 
     def append_rows(self, seq_id: int, k_rows: torch.Tensor, v_rows: torch.Tensor,
-                    positions: np.ndarray) -> int:
+                    positions: np.ndarray, positions_dev: torch.Tensor | None = None) -> int:
         """Fast path with host-known positions (no device sync): rows are valid,
-        belong to seq_id and are in the given position order."""
-        return self._append_rows(seq_id, k_rows, v_rows, np.asarray(positions, np.int64))
+        belong to seq_id and are in the given position order.  ``positions_dev``
+        (int32, on the device, equal to ``positions``) saves the upload."""
+        return self._append_rows(seq_id, k_rows, v_rows, np.asarray(positions, np.int64), positions_dev)
 
     def append_tokens(self, seq_ids, k_rows: torch.Tensor, v_rows: torch.Tensor, positions) -> None:
         """Batched decode append: row j of k_rows/v_rows is one new token of
@@ -176,7 +177,7 @@ class RankKvCache:
         self.pos.index_copy_(0, rows_d, meta_d[0])
         self.seq.index_copy_(0, rows_d, meta_d[1])
 
-    def _append_rows(self, seq_id, k_rows, v_rows, pos_host: np.ndarray) -> int:
+    def _append_rows(self, seq_id, k_rows, v_rows, pos_host: np.ndarray, pos_dev=None) -> int:
         n = int(pos_host.shape[0])
         if n == 0:
             return self.cached_len(seq_id)
@@ -184,11 +185,15 @@ class RankKvCache:
             order = np.argsort(pos_host, kind="stable")
             sel = _lib.h2d(order, self.device)
             k_rows, v_rows, pos_host = k_rows[sel], v_rows[sel], pos_host[order]
+            pos_dev = None if pos_dev is None else pos_dev[sel]
         seg = self._reserve(seq_id, n)
         a = seg.start + seg.length
         self.k[a:a + n].copy_(k_rows.to(self.dtype))
         self.v[a:a + n].copy_(v_rows.to(self.dtype))
-        self.pos[a:a + n].copy_(_lib.h2d(pos_host.astype(np.int32), self.device))
+        if pos_dev is not None:
+            self.pos[a:a + n].copy_(pos_dev)
+        else:
+            self.pos[a:a + n].copy_(_lib.h2d(pos_host.astype(np.int32), self.device))
         self.seq[a:a + n].fill_(int(seq_id))
         seg.length += n
         if pos_host[0] <= seg.max_pos:

@@ -176,17 +176,38 @@ class PeerPartials:
 @dataclass
 class HostStage:
     """Inputs of one host-buffer prefill staged on the device by
-    ``RingAttention.stage_host_inputs`` (copies queued, with ready events)."""
+    ``RingAttention.stage_host_inputs`` (copies queued, with ready events).
+    k / v / q / qp / qs live in one of the ring's rotating staging slots and
+    are valid for exactly one ``pass_kv_prefill_host`` call."""
 
     plan: ShardPlan
-    kb: EmbeddingBlock
-    vb: EmbeddingBlock
+    k: torch.Tensor
+    v: torch.Tensor
     q: torch.Tensor
     qp: torch.Tensor
     qs: torch.Tensor
     splits: list
     kv_ready: torch.cuda.Event
     q_ready: list
+    slot: int
+
+
+def _slot_runs(seg: np.ndarray, seq_off: np.ndarray):
+    """Split a slot range's source-row map (concatenated row index per slot,
+    -1 = padding) into maximal runs: (start, end, sequence, first row in that
+    sequence) for consecutive rows of one sequence, (start, end, -1, 0) for
+    padding.  Vectorised: O(slots) numpy, a Python step per run only."""
+    n = seg.size
+    if n == 0:
+        return []
+    v = seg >= 0
+    si = np.searchsorted(seq_off, np.where(v, seg, 0), side="right") - 1
+    brk = np.ones(n, dtype=bool)
+    brk[1:] = (v[1:] != v[:-1]) | (v[1:] & ((seg[1:] != seg[:-1] + 1) | (si[1:] != si[:-1])))
+    starts = np.flatnonzero(brk)
+    ends = np.append(starts[1:], n)
+    return [(int(j), int(e), int(si[j]) if v[j] else -1, int(seg[j] - seq_off[si[j]]) if v[j] else 0)
+            for j, e in zip(starts, ends)]
 
 
 # ------------------------------------------------------------------ message layouts
@@ -292,21 +313,28 @@ def build_kv_message(plan: ShardPlan, cache: RankKvCache, buf: torch.Tensor | No
 
 
 def append_new_tokens(plan: ShardPlan, rank: int, cache: RankKvCache, k_block: EmbeddingBlock,
-                      v_block: EmbeddingBlock) -> None:
+                      v_block: EmbeddingBlock, slot_pos: torch.Tensor | None = None) -> None:
     """Append this rank's valid new K/V to its cache BEFORE the ring.
-    Positions are host-known from the plan, so no device sync is needed."""
+    Positions are host-known from the plan, so no device sync is needed;
+    ``slot_pos`` (the block's folded int32 slot positions, already on the
+    device) supplies them without an upload."""
     off = 0
     for i, sh in enumerate(plan.sequences):
         loc = plan.rank_local_indices(i, rank)
         slots = np.nonzero(loc >= 0)[0]
         if slots.size:
-            rows = _lib.h2d(slots + off, k_block.data.device)
+            pd = None
             if slots[-1] - slots[0] + 1 == slots.size:  # contiguous: plain slice
                 a, b = off + int(slots[0]), off + int(slots[-1]) + 1
                 kr, vr = k_block.data[a:b], v_block.data[a:b]
+                if slot_pos is not None:
+                    pd = slot_pos[a:b]
             else:
+                rows = _lib.h2d(slots + off, k_block.data.device)
                 kr, vr = k_block.data[rows], v_block.data[rows]
-            cache.append_rows(sh.spec.seq_id, kr, vr, sh.spec.cached_len + loc[slots])
+                if slot_pos is not None:
+                    pd = slot_pos[rows]
+            cache.append_rows(sh.spec.seq_id, kr, vr, sh.spec.cached_len + loc[slots], pd)
         off += loc.size
 
 
@@ -503,16 +531,50 @@ class RingAttention:
             self._bufs[("stream", key)] = s
         return s
 
+    # Host-buffer serving path: staged inputs and device outputs live in
+    # _HOST_SLOTS rotating slots guarded by events, so a request loop
+    # allocates nothing after its first requests (device or page-locked
+    # allocations between stream commands synchronise the device and would
+    # break the copy / compute overlap).
+    _HOST_SLOTS = 2
+
+    def _slot_tensor(self, key, shape, dtype, device) -> torch.Tensor:
+        t = self._bufs.get(key)
+        if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype or t.device != torch.device(device):
+            if t is not None and t.is_cuda:  # copy streams may still read / write the old block
+                for name in ("h2d", "d2h"):
+                    t.record_stream(self._side_stream(name))
+            t = torch.empty(shape, dtype=dtype, device=device)
+            self._bufs[key] = t
+        return t
+
+    def _next_slot(self, kind: str) -> int:
+        """Round-robin over the slots of ``kind`` that are not pending (staged
+        but not yet consumed); a new slot when all are, so staging any number
+        of requests ahead stays correct (steady state: _HOST_SLOTS slots)."""
+        pending = self._bufs.setdefault(("slotpending", kind), set())
+        n_slots = self._bufs.get(("slotcount", kind), self._HOST_SLOTS)
+        ctr = self._bufs.get(("slotctr", kind), 0)
+        for i in range(n_slots):
+            c = (ctr + i) % n_slots
+            if c not in pending:
+                break
+        else:
+            c = n_slots
+            self._bufs[("slotcount", kind)] = n_slots + 1
+        self._bufs[("slotctr", kind)] = c + 1
+        return c
+
     def stage_host_inputs(self, plan: ShardPlan, q_host, k_host, v_host, cfg: GqaConfig, device,
                           n_sub: int | None = None) -> "HostStage":
         """Queue the host->device copies of one prefill's inputs on the copy
         stream: K/V of this rank's chunks first, then its query slots in ranges
         (``n_sub``, default one per 8192 slots, at most 16), each range with a
-        ready event.  The device buffers come from the copy stream's own pool,
-        so staging may run ahead of the compute stream (e.g. the next request
-        while this one computes); the host tensors must stay unchanged until
-        the copies have run."""
-        from .sharding import _host_index_map, materialize_rank_block
+        ready event.  The device buffers are one of two rotating staging slots
+        (the copies into a slot wait for the compute that last read it), so
+        staging may run one request ahead of the compute stream; the host
+        tensors must stay unchanged until the copies have run."""
+        from .sharding import _host_index_map
 
         k = self.comm.rank
         s_in = self._side_stream("h2d")
@@ -523,41 +585,49 @@ class RingAttention:
             n_sub = min(16, max(1, S // 8192))
         step = max(256, -(-S // max(n_sub, 1)) // 256 * 256)
         splits = [(a, min(S, a + step)) for a in range(0, S, step)]
+        q_host, k_host, v_host = ([t if isinstance(t, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(t))
+                                   for t in src] for src in (q_host, k_host, v_host))
+        for name, src in (("q", q_host), ("k", k_host), ("v", v_host)):
+            for sh, t in zip(plan.sequences, src):
+                if t.shape[0] != sh.spec.new_len:
+                    raise ValueError(f"sequence {sh.spec.seq_id}: {name} array has {t.shape[0]} rows, "
+                                     f"expected new_len={sh.spec.new_len}")
+        kvh = k_host[0].shape[1] if len(k_host) else cfg.n_kv_heads
+        seq_off = np.cumsum([0] + [t.shape[0] for t in q_host])  # idx rows are concatenated
+        slot = self._next_slot("stage")
+        self._bufs[("slotpending", "stage")].add(slot)
+        q = self._slot_tensor(("stage", slot, "q"), (S, H, D), torch.bfloat16, device)
+        kd = self._slot_tensor(("stage", slot, "k"), (S, kvh, D), torch.bfloat16, device)
+        vd = self._slot_tensor(("stage", slot, "v"), (S, kvh, D), torch.bfloat16, device)
+        qp = self._slot_tensor(("stage", slot, "qp"), (S,), torch.int32, device)
+        qs = self._slot_tensor(("stage", slot, "qs"), (S,), torch.int32, device)
+        free = self._bufs.get(("stage", slot, "free"))
         with torch.cuda.stream(s_in):
-            kb = materialize_rank_block(plan, k, list(k_host), device)
-            vb = materialize_rank_block(plan, k, list(v_host), device)
-            kv_ready = torch.cuda.Event()
+            if free is not None:  # the compute that last read this slot is done
+                s_in.wait_event(free)
+
+            def fill(dst, srcs, a, b):
+                flat = dst.view(dst.shape[0], -1)
+                for j, e, si, lo in _slot_runs(idx[a:b], seq_off):
+                    if si < 0:
+                        flat[a + j:a + e].zero_()
+                    else:
+                        flat[a + j:a + e].copy_(srcs[si].reshape(srcs[si].shape[0], -1)[lo:lo + e - j],
+                                                non_blocking=True)
+
+            fill(kd, k_host, 0, S)
+            fill(vd, v_host, 0, S)
+            kv_ready = torch.cuda.Event(enable_timing=True)  # timing: tools/e2e_loop_ranges.py
             kv_ready.record(s_in)
-            qp = _lib.h2d(posv.astype(np.int32), device)
-            qs = _lib.h2d(seqv.astype(np.int32), device)
-            q = torch.empty((S, H, D), dtype=torch.bfloat16, device=device)
-            srcs = [t.reshape(t.shape[0], -1) for t in q_host]
-            seq_off = np.cumsum([0] + [t.shape[0] for t in srcs])  # idx rows are concatenated
-            qf = q.view(S, -1)
+            _lib.h2d(posv.astype(np.int32), device, out=qp)
+            _lib.h2d(seqv.astype(np.int32), device, out=qs)
             q_ready = []
             for a, b in splits:
-                seg = idx[a:b]
-                # contiguous runs of valid source rows; padding slots zeroed
-                j = 0
-                while j < seg.size:
-                    if seg[j] < 0:
-                        e = j
-                        while e < seg.size and seg[e] < 0:
-                            e += 1
-                        qf[a + j:a + e].zero_()
-                    else:
-                        g = int(seg[j])
-                        si = int(np.searchsorted(seq_off, g, side="right")) - 1
-                        e = j + 1
-                        while e < seg.size and seg[e] == seg[e - 1] + 1 and seg[e] < seq_off[si + 1]:
-                            e += 1
-                        lo = g - int(seq_off[si])
-                        qf[a + j:a + e].copy_(srcs[si][lo:lo + e - j], non_blocking=True)
-                    j = e
-                ev = torch.cuda.Event()
+                fill(q, q_host, a, b)
+                ev = torch.cuda.Event(enable_timing=True)
                 ev.record(s_in)
                 q_ready.append(ev)
-        return HostStage(plan, kb, vb, q, qp, qs, splits, kv_ready, q_ready)
+        return HostStage(plan, kd, vd, q, qp, qs, splits, kv_ready, q_ready, slot)
 
     def join_host_copies(self) -> None:
         """Order the caller's stream after every queued device->host copy."""
@@ -577,7 +647,9 @@ class RingAttention:
         ``stage_host_inputs`` (or taken from ``staged``, queued earlier), every
         ring step runs one attention launch per query range as it lands, and
         each range's final rows go back on a second copy stream as soon as its
-        last launch is queued.  With ``join`` (default) the caller's stream is
+        last launch is queued.  The device result lives in one of two rotating
+        output slots (the first launch into a slot waits for the copies that
+        last read it).  With ``join`` (default) the caller's stream is
         ordered after those copies; a serving loop that stages the next
         request meanwhile passes ``join=False`` and calls ``join_host_copies``
         once at the end."""
@@ -589,14 +661,16 @@ class RingAttention:
                                                                       n_sub)
         if st.plan is not plan and st.plan != plan:
             raise ValueError("staged inputs belong to a different plan")
-        for t in (st.kb.data, st.vb.data, st.q, st.qp, st.qs):  # made on the copy stream, read here
-            t.record_stream(cur)
         H, D = cfg.n_query_heads, cfg.head_dim
         S = st.q.shape[0]
-        out = torch.empty((S, H, D), dtype=torch.float32, device=dev)
-        lse = torch.empty((S, H), dtype=torch.float32, device=dev)
+        oslot = self._next_slot("out")
+        out = self._slot_tensor(("out", oslot, "o"), (S, H, D), torch.float32, dev)
+        lse = self._slot_tensor(("out", oslot, "lse"), (S, H), torch.float32, dev)
+        ofree = self._bufs.get(("out", oslot, "free"))
+        if ofree is not None:  # the D2H copies that last read this slot are done
+            cur.wait_event(ofree)
         cur.wait_event(st.kv_ready)
-        append_new_tokens(plan, k, cache, st.kb, st.vb)
+        append_new_tokens(plan, k, cache, st.k, st.v, slot_pos=st.qp)
         lay = KvLayout(kv_message_len(plan), cache.n_kv_heads, cache.head_dim)
         msg = self._buf(("kv", "local"), lay.nbytes, dev)
         build_kv_message(plan, cache, msg)
@@ -613,8 +687,13 @@ class RingAttention:
 
         self.pass_kv(st.q, st.qp, st.qs, lay, msg, cfg, out, lse, cache.dtype, q_splits=splits,
                      q_ready=st.q_ready, on_final=on_final)
-        for t in (out, lse):
-            t.record_stream(s_out)
+        done = torch.cuda.Event()
+        done.record(cur)
+        self._bufs[("stage", st.slot, "free")] = done  # staging slot may be refilled
+        self._bufs[("slotpending", "stage")].discard(st.slot)
+        ofree = torch.cuda.Event()
+        ofree.record(s_out)
+        self._bufs[("out", oslot, "free")] = ofree
         if join:
             cur.wait_stream(s_out)
 

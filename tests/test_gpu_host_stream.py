@@ -92,3 +92,50 @@ def test_staged_pipeline_two_requests():
     torch.cuda.synchronize()
     for (oh, lh), (ro, rl) in zip(outs, refs):
         assert torch.equal(oh, ro) and torch.equal(lh, rl)
+
+
+@pytest.mark.parametrize("ahead", [1, 3, 6])
+def test_staged_pipeline_slot_reuse(ahead):
+    """Six requests with distinct data and alternating shapes (the rotating
+    staging / output slots are re-used and re-allocated), staged ``ahead``
+    requests before their compute (more than the two steady-state slots:
+    pending slots are never overwritten); every result equals the device path."""
+    from paper_2411_01783_b200.attention import GqaConfig
+    from paper_2411_01783_b200.kv_cache import RankKvCache
+    from paper_2411_01783_b200.ring import RingAttention, _LocalComm
+    from paper_2411_01783_b200.sharding import SequenceSpec, materialize_rank_block, plan_full_prefill
+
+    hq, hkv, D = 8, 2, 128
+    cfg = GqaConfig(hq, hkv, D)
+    g = torch.Generator().manual_seed(11)
+    mk = lambda *s: torch.randn(*s, generator=g).to(torch.bfloat16).pin_memory()
+    reqs = []
+    for i in range(6):
+        T = (3000, 1100)[(i // 2) % 2]
+        plan = plan_full_prefill([SequenceSpec(1, 0, T)], 1)
+        reqs.append((plan, [mk(T, hq, D)], [mk(T, hkv, D)], [mk(T, hkv, D)]))
+    ring = RingAttention(_LocalComm(0, 1))
+    refs = []
+    for plan, qh, kh, vh in reqs:
+        r = ring.pass_kv_prefill(plan, RankKvCache(hkv, D, capacity_tokens=256),
+                                 materialize_rank_block(plan, 0, [qh[0].cuda()]),
+                                 materialize_rank_block(plan, 0, [kh[0].cuda()]),
+                                 materialize_rank_block(plan, 0, [vh[0].cuda()]), cfg)
+        refs.append((r.output.data.cpu(), r.lse.cpu()))
+    torch.cuda.synchronize()
+    dev = torch.device("cuda")
+    staged = [ring.stage_host_inputs(*reqs[j], cfg, dev) for j in range(min(ahead, len(reqs)))]
+    outs = []
+    for i, (plan, qh, kh, vh) in enumerate(reqs):
+        S = plan.total_query_slots()
+        oh = torch.full((S, hq, D), float("nan")).pin_memory()
+        lh = torch.full((S, hq), float("nan")).pin_memory()
+        ring.pass_kv_prefill_host(plan, RankKvCache(hkv, D, capacity_tokens=256), qh, kh, vh, cfg, oh, lh,
+                                  staged=staged[i], join=False)
+        outs.append((oh, lh))
+        if i + ahead < len(reqs):
+            staged.append(ring.stage_host_inputs(*reqs[i + ahead], cfg, dev))
+    ring.join_host_copies()
+    torch.cuda.synchronize()
+    for i, ((oh, lh), (ro, rl)) in enumerate(zip(outs, refs)):
+        assert torch.equal(oh, ro) and torch.equal(lh, rl), i
