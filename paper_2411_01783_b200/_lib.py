@@ -191,25 +191,25 @@ def _meta_stream(device):
     return s
 
 
-def h2d(arr, device, out=None):
+def h2d(arr, device, out=None, side=False):
     """Host array -> device tensor (or into ``out``) without a host/device
     sync: staged through the persistent pinned ring (_PinnedRing) and copied
     with non_blocking=True.  Arrays above 8 MB get a dedicated pinned block
     instead.  A pageable source would make the copy wait for all earlier work
     on the stream.
 
-    Without ``out`` the copy runs on a dedicated metadata stream that depends
-    on nothing, and the current stream waits for it: copy engines serve
-    host->device copies in submission order, so a small copy ordered behind
-    the compute stream's earlier work would otherwise queue behind any large
-    transfer submitted meanwhile (e.g. the next request's staged inputs).
-    With ``out`` (the destination may still be in use) the copy is ordered on
-    the current stream."""
+    ``side=True`` (without ``out``) runs the copy on a dedicated metadata
+    stream that depends on nothing and makes the current stream wait for it:
+    copy engines serve host->device copies in submission order, so a small
+    copy ordered behind the compute stream's earlier work would otherwise
+    queue behind any large transfer submitted meanwhile (e.g. the next
+    request's staged inputs).  It costs a few tens of microseconds of host
+    time, so latency-bound paths (decode) keep the default."""
     global _RING
     import numpy as np
     import torch
 
-    if out is None and torch.device(device).type == "cuda" and not torch.cuda.is_current_stream_capturing():
+    if side and out is None and torch.device(device).type == "cuda" and not torch.cuda.is_current_stream_capturing():
         cur = torch.cuda.current_stream(device)
         ms = _meta_stream(device)
         with torch.cuda.stream(ms):

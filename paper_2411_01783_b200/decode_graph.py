@@ -160,7 +160,7 @@ class GraphedDecode:
             self.k_in[:m].copy_(k_tok[:m])
             self.v_in[:m].copy_(v_tok[:m])
         meta = self._host_meta(mine, positions)
-        self.meta.copy_(_lib.h2d(meta, self.cache.device), non_blocking=True)
+        _lib.h2d(meta, self.cache.device, out=self.meta)  # ordered after the previous replay
         ptrs = (self.cache.k.data_ptr(), self.cache.v.data_ptr(), self.cache.pos.data_ptr(),
                 self.cache.seq.data_ptr())
         if self.graph is None or ptrs != self._arena_ptr:

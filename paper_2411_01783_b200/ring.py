@@ -330,7 +330,7 @@ def append_new_tokens(plan: ShardPlan, rank: int, cache: RankKvCache, k_block: E
                 if slot_pos is not None:
                     pd = slot_pos[a:b]
             else:
-                rows = _lib.h2d(slots + off, k_block.data.device)
+                rows = _lib.h2d(slots + off, k_block.data.device, side=True)
                 kr, vr = k_block.data[rows], v_block.data[rows]
                 if slot_pos is not None:
                     pd = slot_pos[rows]
