@@ -53,6 +53,7 @@ struct AttnParams {
   const __nv_bfloat16* q;  // v7: query rows are read directly (into TMEM)
   int64_t q_stride;        // elements between consecutive query rows
   long long* trace;  // RCP_TRACE builds only: per-CTA role timestamps (clock64)
+  int* item_ctr;     // v9: work-item counter (workspace, zeroed by active_list_kernel)
 };
 
 #ifndef RCP_TRACE
@@ -217,10 +218,10 @@ __device__ __forceinline__ void arrive_leader(uint64_t* bar) {
 
 // ---- variants (attn_variants.cu)
 // Key-block rows of a version's tile summaries / TMA boxes.
-inline int attn_key_rows(int version) { return (version == 4 || version == 7) ? 64 : 128; }
+inline int attn_key_rows(int version) { return (version == 4 || version == 7 || version == 9) ? 64 : 128; }
 inline int attn_k_box_rows(int version) { return version == 6 ? 128 : 64; }
-inline int attn_v_box_rows(int version) { return (version == 4 || version == 7) ? 64 : 128; }
-// Launch variant `version` (5..8) over n_pairs_heads = (query-tile pairs) x Hq.
+inline int attn_v_box_rows(int version) { return (version == 4 || version == 7 || version == 9) ? 64 : 128; }
+// Launch variant `version` (5..9) over n_pairs_heads = (query-tile pairs) x Hq.
 int attn_variant_launch(int version, const AttnParams& prm, int64_t n_pairs_heads, cudaStream_t st);
 
 }  // namespace rcp

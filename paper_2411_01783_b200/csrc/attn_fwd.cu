@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(256) active_list_kernel(const TileSum* __restr
     __syncthreads();
   }
   if (threadIdx.x == 0) act_n[qb] = base;
+  if (qb == 0 && threadIdx.x == 0) act_n[gridDim.x] = 0;  // v9's work-item counter (workspace slack)
 }
 
 __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ AttnParams p) {
@@ -559,13 +560,14 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
   // v4 (1-CTA, 64-key blocks) is the default: it measured best on the power-
   // capped B200s ("Attention kernel versions").  RCP_ATTN_VERSION=5
   // (CTA pairs), =6 (1-CTA, 128-key blocks, split softmax), =7 (Q in TMEM,
-  // TS-form S) and =8 (CTA pairs, alternate-block softmax groups) are kept for
-  // A/B measurements; all pass the same parity tests.
+  // TS-form S), =8 (CTA pairs, alternate-block softmax groups) and =9
+  // (persistent v4) are kept for A/B measurements; all pass the same parity
+  // tests.
   static int version = -1;
   if (version < 0) {
     const char* e = getenv("RCP_ATTN_VERSION");
     const int v = e ? atoi(e) : 4;
-    version = (v == 5 || v == 6 || v == 7 || v == 8) ? v : 4;
+    version = (v >= 5 && v <= 9) ? v : 4;
   }
   const int krows = attn_key_rows(version);
   AttnParams prm;
@@ -596,6 +598,7 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
   RCP_CUDA(cudaGetLastError());
   prm.act = act;
   prm.act_n = act_n;
+  prm.item_ctr = act_n + n_qblk;
   prm.q_pos = q_pos;
   prm.q_seq = q_seq;
   prm.k_pos = k_pos;

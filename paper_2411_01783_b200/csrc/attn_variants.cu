@@ -1536,6 +1536,416 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 
+
+// ======================================================================
+// v9: persistent v4.  One CTA per SM streams (query block, head) items in
+// v4's heavy-first order, claimed dynamically: the producer lane takes the
+// next item from a global counter and hands it to the MMA and softmax warps
+// through a 4-deep shared-memory ring (full / empty mbarriers); the roles keep
+// their barrier phases across items — S/P/K/V phases from a global block
+// counter, Q / O phases from the count of non-empty items — so the next
+// item's Q load, first K/V loads and first two S MMAs overlap the current
+// item's drain and epilogue, and TMEM allocation, barrier init and descriptor
+// prefetch happen once per CTA.  Two extra hand-offs: bar_qfree (MMA commit
+// after an item's last S: Q smem may be reloaded) and bar_ofree (the tile's
+// softmax threads read O out: the next item's first PV may overwrite it).
+// ======================================================================
+__global__ void __launch_bounds__(kThreads, 1) attn_fwd_v9_kernel(const __grid_constant__ AttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem =
+      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + 2 * kQTileBytes;
+
+  __shared__ uint64_t bar_q, bar_qfree, bar_full[kSlots], bar_empty[kSlots];
+  __shared__ uint64_t bar_s[2][2], bar_p[2][2], bar_pv[2], bar_o[2], bar_ofree[2];
+  constexpr int kItemSlots = 4;
+  __shared__ uint64_t bar_item_full[kItemSlots], bar_item_empty[kItemSlots];
+  __shared__ int item_buf[kItemSlots];
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = static_cast<int>(warp_id());
+  const int per_kv = p.n_qblk * p.group;
+  // consumer side of the item ring: k-th item of this CTA (>= n_items: done)
+  // (whole_warp: all 32 lanes call, lane 0 releases the slot after every
+  // lane has read it; otherwise a single elected lane reads and releases)
+  auto next_item = [&](uint32_t k, bool whole_warp) -> int {
+    const uint32_t sl = k % kItemSlots;
+    mbar_wait(&bar_item_full[sl], (k / kItemSlots) & 1);
+    const int item = reinterpret_cast<volatile int*>(item_buf)[sl];
+    if (whole_warp) __syncwarp();
+    if (!whole_warp || (threadIdx.x & 31) == 0) mbar_arrive(&bar_item_empty[sl]);
+    return item;
+  };
+  const int n_items = per_kv * p.hkv;
+  auto item_coords = [&](int item, int& qblk, int& head, int& kvh) {
+    kvh = item / per_kv;
+    const int rem = item - kvh * per_kv;
+    qblk = p.n_qblk - 1 - rem / p.group;
+    head = kvh * p.group + rem % p.group;
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_q, 1);
+    mbar_init(&bar_qfree, 1);
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(&bar_full[s], 1);
+      mbar_init(&bar_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&bar_s[t][0], 1);
+      mbar_init(&bar_s[t][1], 1);
+      mbar_init(&bar_p[t][0], 128);
+      mbar_init(&bar_p[t][1], 128);
+      mbar_init(&bar_pv[t], 1);
+      mbar_init(&bar_o[t], 1);
+      mbar_init(&bar_ofree[t], 128);
+    }
+    for (int i = 0; i < kItemSlots; ++i) {
+      mbar_init(&bar_item_full[i], 1);
+      mbar_init(&bar_item_empty[i], 1 + 8);  // MMA lane + lane 0 of each softmax warp
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      tma_prefetch_desc(&p.tm_q);
+      tma_prefetch_desc(&p.tm_k);
+      tma_prefetch_desc(&p.tm_v);
+      const uint64_t pol_q = policy_evict_first();
+      const uint64_t pol_kv = policy_evict_last();
+      uint32_t ld = 0, qi = 0;
+      for (uint32_t k = 0;; ++k) {
+        const uint32_t sl = k % kItemSlots;
+        mbar_wait(&bar_item_empty[sl], ((k / kItemSlots) & 1) ^ 1);
+        const int item = atomicAdd(p.item_ctr, 1);
+        reinterpret_cast<volatile int*>(item_buf)[sl] = item;
+        mbar_arrive(&bar_item_full[sl]);
+        if (item >= n_items) break;
+        int qblk, head, kvh;
+        item_coords(item, qblk, head, kvh);
+        const int n = __ldg(p.act_n + qblk);
+        if (n == 0) continue;
+        const uint32_t* act = p.act + static_cast<int64_t>(qblk) * p.n_kblocks;
+        if (qi > 0) mbar_wait(&bar_qfree, (qi - 1) & 1);  // previous item's S MMAs read Q
+        mbar_arrive_expect_tx(&bar_q, 2 * kQTileBytes);
+        for (int t = 0; t < 2; ++t)
+          for (int h = 0; h < 2; ++h)
+            tma_load_2d(sQ + t * kQTileBytes + h * kQBoxBytes, &p.tm_q, &bar_q, head * kD + h * 64,
+                        (2 * qblk + t) * kQRows, pol_q);
+        uint32_t e_next = __ldg(act);
+        for (int it = 0; it < n; ++it) {
+          const int j = act_j(e_next);
+          if (it + 1 < n) e_next = __ldg(act + it + 1);
+#pragma unroll
+          for (int kv = 0; kv < 2; ++kv, ++ld) {
+            const uint32_t slot = ld % kSlots, ph = (ld / kSlots) & 1;
+            mbar_wait(&bar_empty[slot], ph ^ 1);
+            mbar_arrive_expect_tx(&bar_full[slot], kKVBytes);
+            const CUtensorMap* map = kv ? &p.tm_v : &p.tm_k;
+            for (int h = 0; h < 2; ++h)
+              tma_load_2d(sKV + slot * kKVBytes + h * kKVBoxBytes, map, &bar_full[slot],
+                          kvh * kD + h * 64, j * kKRows, pol_kv);
+          }
+        }
+        ++qi;
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      const uint32_t idesc_s = make_idesc_bf16_f32(kQRows, kKRows, 0, 0);
+      const uint32_t idesc_o = make_idesc_bf16_f32(kQRows, kD, 0, 1);
+      const uint32_t q_lo = sw128_desc_lo(smem_u32(sQ), 16);
+      const uint32_t k_lo = sw128_desc_lo(smem_u32(sKV), 16);
+      const uint32_t v_lo = sw128_desc_lo(smem_u32(sKV), kKVBoxBytes);
+      auto wait_load = [&](uint32_t ld) {
+        mbar_wait(&bar_full[ld % kSlots], (ld / kSlots) & 1);
+        tc_fence_after();
+      };
+      auto issue_s = [&](int t, int buf, uint32_t ld) {
+        const uint32_t qa = q_lo + ((t * kQTileBytes) >> 4);
+        const uint32_t ka = k_lo + (((ld % kSlots) * kKVBytes) >> 4);
+        const uint32_t d = tmem + kTmemS + (2 * t + buf) * kKRows;
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk)
+          mma_ss_lo(d, qa + (((kk >> 2) * kQBoxBytes + (kk & 3) * 32) >> 4),
+                    ka + (((kk >> 2) * kKVBoxBytes + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
+      };
+      auto issue_pv = [&](int t, int buf, uint32_t ld, bool acc) {
+        const uint32_t va = v_lo + (((ld % kSlots) * kKVBytes) >> 4);
+        const uint32_t pa = tmem + kTmemS + (2 * t + buf) * kKRows;
+#pragma unroll
+        for (int kk = 0; kk < kKRows / 16; ++kk)
+          mma_ts_lo(tmem + kTmemO + t * kD, pa + kk * 8, va + ((kk * 2048) >> 4), idesc_o,
+                    (acc || kk > 0) ? 1u : 0u);
+      };
+      uint32_t g0 = 0, qi = 0;  // global index of the item's first block; non-empty items so far
+      for (uint32_t k = 0;; ++k) {
+        const int item = next_item(k, false);
+        if (item >= n_items) break;
+        int qblk, head, kvh;
+        item_coords(item, qblk, head, kvh);
+        const int n = __ldg(p.act_n + qblk);
+        if (n == 0) continue;
+        mbar_wait(&bar_q, qi & 1);
+        tc_fence_after();
+        // prologue: S(g0), S(g0 + 1) for both tiles
+        {
+          const int b0 = g0 & 1;
+          wait_load(2 * g0);
+          issue_s(0, b0, 2 * g0);
+          mma_commit(&bar_s[0][b0]);
+          issue_s(1, b0, 2 * g0);
+          mma_commit(&bar_s[1][b0]);
+          mma_commit(&bar_empty[(2 * g0) % kSlots]);
+          if (n > 1) {
+            const int b1 = (g0 + 1) & 1;
+            wait_load(2 * (g0 + 1));
+            issue_s(0, b1, 2 * (g0 + 1));
+            mma_commit(&bar_s[0][b1]);
+            issue_s(1, b1, 2 * (g0 + 1));
+            mma_commit(&bar_s[1][b1]);
+            mma_commit(&bar_empty[(2 * (g0 + 1)) % kSlots]);
+          }
+          if (n <= 2) mma_commit(&bar_qfree);  // every S of this item issued
+        }
+        for (int it = 0; it < n; ++it) {
+          const uint32_t g = g0 + it;
+          const int buf = g & 1;
+          const uint32_t ph = (g >> 1) & 1;
+          const bool last = it + 1 == n, has2 = it + 2 < n;
+          const uint32_t ldv = 2 * g + 1, ldk2 = 2 * (g + 2);
+          wait_load(ldv);
+          for (int t = 0; t < 2; ++t) {
+            mbar_wait(&bar_p[t][buf], ph);
+            tc_fence_after();
+            if (it == 0 && qi > 0) {  // the previous item's epilogue has read O_t
+              mbar_wait(&bar_ofree[t], (qi - 1) & 1);
+              tc_fence_after();
+            }
+            issue_pv(t, buf, ldv, it > 0);
+            mma_commit(last ? &bar_o[t] : &bar_pv[t]);
+            if (t == 1) mma_commit(&bar_empty[ldv % kSlots]);
+            if (has2) {
+              if (t == 0) wait_load(ldk2);
+              issue_s(t, buf, ldk2);
+              mma_commit(&bar_s[t][buf]);
+              if (t == 1) {
+                mma_commit(&bar_empty[ldk2 % kSlots]);
+                if (it + 3 == n) mma_commit(&bar_qfree);  // S(g0 + n - 1) was the item's last S
+              }
+            }
+          }
+        }
+        g0 += n;
+        ++qi;
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax + epilogue
+    const int w = (warp - 4) >> 2;
+    const int t = static_cast<int>(threadIdx.x) - 128 - 128 * w;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+    const uint32_t o_addr = lane_base + kTmemO + w * kD;
+    const float sl2 = p.scale_log2;
+    const uint64_t sl2x2 = f2(sl2, sl2);
+    const bool merge = p.mode == RCP_MODE_MERGE;
+    uint32_t g0 = 0, qi = 0, pvb = 0;  // global block base, non-empty items, bar_pv commits so far
+    for (uint32_t k = 0;; ++k) {
+      const int item = next_item(k, true);
+      if (item >= n_items) break;
+      int qblk, head, kvh;
+      item_coords(item, qblk, head, kvh);
+      const int row = (2 * qblk + w) * kQRows + t;
+      const bool row_ok = row < p.tq;
+      const int my_pos = row_ok ? __ldg(p.q_pos + row) : -1;
+      const int my_seq = row_ok ? __ldg(p.q_seq + row) : RCP_SEQ_PAD_Q;
+      float m = -INFINITY, l = 0.f;
+      const int n = __ldg(p.act_n + qblk);
+      const uint32_t* act = p.act + static_cast<int64_t>(qblk) * p.n_kblocks;
+      uint32_t e_next = n > 0 ? __ldg(act) : 0u;
+      int it = 0;
+      for (; it < n; ++it) {
+        const uint32_t g = g0 + it;
+        const int buf = g & 1;
+        const uint32_t s_addr = lane_base + kTmemS + (2 * w + buf) * kKRows;
+        const uint32_t e = e_next;
+        if (it + 1 < n) e_next = __ldg(act + it + 1);
+        const int j = act_j(e);
+        const int cls = act_cls(e, w);
+        mbar_wait(&bar_s[w][buf], (g >> 1) & 1);
+        tc_fence_after();
+        if (cls != kTileEmpty) {
+          uint32_t sr[64];
+          tmem_ld32(s_addr, sr);
+          tmem_ld32(s_addr + 32, sr + 32);
+          tmem_ld_wait();
+          float s[64];
+#pragma unroll
+          for (int c = 0; c < 64; ++c) s[c] = __uint_as_float(sr[c]);
+          if (cls == kTilePartial) {
+            const int base = j * kKRows;
+            if (base + kKRows <= p.tk) {
+              const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + base);
+              const int4* ks4 = reinterpret_cast<const int4*>(p.k_seq + base);
+#pragma unroll
+              for (int c4 = 0; c4 < 16; ++c4) {
+                const int4 kp = __ldg(kp4 + c4), kq = __ldg(ks4 + c4);
+                if (!(kq.x == my_seq && kp.x <= my_pos)) s[4 * c4 + 0] = -INFINITY;
+                if (!(kq.y == my_seq && kp.y <= my_pos)) s[4 * c4 + 1] = -INFINITY;
+                if (!(kq.z == my_seq && kp.z <= my_pos)) s[4 * c4 + 2] = -INFINITY;
+                if (!(kq.w == my_seq && kp.w <= my_pos)) s[4 * c4 + 3] = -INFINITY;
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < 64; ++c) {
+                const int kidx = base + c;
+                const bool ok = kidx < p.tk && __ldg(p.k_seq + kidx) == my_seq &&
+                                __ldg(p.k_pos + kidx) <= my_pos;
+                if (!ok) s[c] = -INFINITY;
+              }
+            }
+          }
+          float m8[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m8[k] = s[k];
+#pragma unroll
+          for (int c = 8; c < 64; c += 8)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) m8[k] = fmaxf(m8[k], s[c + k]);
+          const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                                 fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+          const float m_old = m;
+          const float m_new = fmaxf(m, mx * sl2);
+          const bool need = m_new > m + kRescaleThreshold;
+          if (need) m = m_new;
+          const float m_use = (m == -INFINITY) ? 0.f : m;
+          const uint64_t negm2 = f2(-m_use, -m_use);
+          uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+          uint32_t pk[32];
+          if (cls == kTileFull) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float2 x = unf2(ffma2(f2(s[2 * i], s[2 * i + 1]), sl2x2, negm2));
+              float p0, p1;
+              if ((i & 7) < kPolyPairsPer8) {
+                const float2 pp = ex2_poly_x2(x.x, x.y);
+                p0 = pp.x;
+                p1 = pp.y;
+              } else {
+                p0 = ex2_approx(x.x);
+                p1 = ex2_approx(x.y);
+              }
+              acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
+              pk[i] = pack_bf16x2(p0, p1);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float2 x = unf2(ffma2(f2(s[2 * i], s[2 * i + 1]), sl2x2, negm2));
+              const float p0 = ex2_approx(x.x), p1 = ex2_approx(x.y);
+              acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
+              pk[i] = pack_bf16x2(p0, p1);
+            }
+          }
+          tmem_st32(s_addr, pk);
+          const float2 a01 = unf2(fadd2(acc2[0], acc2[1]));
+          const float2 a23 = unf2(fadd2(acc2[2], acc2[3]));
+          const float sum = (a01.x + a01.y) + (a23.x + a23.y);
+          const float f = (need && m_old != -INFINITY) ? ex2_approx(m_old - m) : 1.0f;
+          l = (m_old == -INFINITY ? 0.f : l * f) + sum;
+          if (__any_sync(0xffffffffu, f != 1.0f && it > 0)) {
+            mbar_wait(&bar_pv[w], (pvb + it - 1) & 1);  // PV_t of the previous block landed
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < kD; c += 32) {
+              uint32_t r[32];
+              tmem_ld32(o_addr + c, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
+              tmem_st32(o_addr + c, r);
+            }
+          }
+        } else {
+          uint32_t pk[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) pk[i] = 0u;
+          tmem_st32(s_addr, pk);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&bar_p[w][buf]);
+      }
+
+      // epilogue: O / l, LSE, optional merge into the running (O, LSE)
+      if (n > 0) {
+        mbar_wait(&bar_o[w], qi & 1);
+        tc_fence_after();
+      }
+      if (!(merge && n == 0)) {
+        const bool has = l > 0.f;
+        const float inv = has ? 1.0f / l : 0.f;
+        const float lse_new = has ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+        float* orow = p.o + (static_cast<int64_t>(row) * p.hq + head) * kD;
+        float* lrow = p.lse + static_cast<int64_t>(row) * p.hq + head;
+        MergeW mw;
+        mw.lse = lse_new;
+        mw.wa = 0.f;
+        mw.wb = 1.f;
+        if (merge && row_ok) mw = merge_weights(__ldg(lrow), lse_new);
+#pragma unroll
+        for (int c = 0; c < kD; c += 32) {
+          uint32_t r[32];
+          if (n > 0) {
+            tmem_ld32(o_addr + c, r);
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = 0u;
+          }
+          if (row_ok) {
+            float4* dst = reinterpret_cast<float4*>(orow + c);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              float4 v = make_float4(__uint_as_float(r[4 * i]) * inv, __uint_as_float(r[4 * i + 1]) * inv,
+                                     __uint_as_float(r[4 * i + 2]) * inv,
+                                     __uint_as_float(r[4 * i + 3]) * inv);
+              if (merge) {
+                const float4 a = dst[i];
+                v = make_float4(merge_val(a.x, v.x, mw), merge_val(a.y, v.y, mw),
+                                merge_val(a.z, v.z, mw), merge_val(a.w, v.w, mw));
+              }
+              dst[i] = v;
+            }
+          }
+        }
+        if (row_ok) *lrow = merge ? mw.lse : lse_new;
+      }
+      if (n > 0) {
+        tc_fence_before();
+        mbar_arrive(&bar_ofree[w]);  // O_t read out: the next item's first PV may overwrite it
+        g0 += n;
+        pvb += n - 1;
+        ++qi;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 int attn_variant_launch(int version, const AttnParams& prm, int64_t grid, cudaStream_t st) {
   const unsigned g = static_cast<unsigned>(grid);
   if (version == 5) {
@@ -1570,6 +1980,19 @@ int attn_variant_launch(int version, const AttnParams& prm, int64_t grid, cudaSt
       attr = true;
     }
     attn_fwd_v8_kernel<<<2 * g, kThreads, kSmem2Bytes, st>>>(prm);
+  } else if (version == 9) {
+    static bool attr = false;
+    static int n_sm = 0;
+    if (!attr) {
+      RCP_CUDA(cudaFuncSetAttribute(attn_fwd_v9_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kSmemBytes));
+      int dev = 0;
+      RCP_CUDA(cudaGetDevice(&dev));
+      RCP_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+      attr = true;
+    }
+    const unsigned gp = static_cast<unsigned>(grid < n_sm ? grid : n_sm);
+    attn_fwd_v9_kernel<<<gp, kThreads, kSmemBytes, st>>>(prm);
   } else {
     set_error("unknown attention kernel version %d", version);
     return RCP_ERR_INVALID;
