@@ -139,19 +139,25 @@ class _PinnedRing:
         self.cap = nbytes
         self.head = 0
         self.live = collections.deque()  # (start, end, event), allocation order
+        self.free_events = []            # retired events, re-recorded instead of created
+
+    def _retire(self, ev) -> None:
+        self.free_events.append(ev)
 
     def take(self, n: int):
         n = (n + 255) // 256 * 256
         if self.head + n > self.cap:
             self.head = 0
         a, b = self.head, self.head + n
-        while self.live and self.live[0][2].query():  # retire completed copies
-            self.live.popleft()
-        if any(s < b and a < e for s, e, _ in self.live):
+        if len(self.live) > 32:  # retire completed copies (lazily: query costs host time)
+            while self.live and self.live[0][2].query():
+                self._retire(self.live.popleft()[2])
+        if self.live and any(s < b and a < e for s, e, _ in self.live):
             keep = type(self.live)()
             for s, e, ev in self.live:
                 if s < b and a < e:
                     ev.synchronize()  # host a whole arena ahead: wait for that copy
+                    self._retire(ev)
                 else:
                     keep.append((s, e, ev))
             self.live = keep
@@ -161,7 +167,7 @@ class _PinnedRing:
     def commit(self, a: int, b: int) -> None:
         import torch
 
-        ev = torch.cuda.Event()
+        ev = self.free_events.pop() if self.free_events else torch.cuda.Event()
         ev.record()
         self.live.append((a, b, ev))
 
