@@ -294,8 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       if (t == 0) TRACE(2 + 2 * w, it);
       if (cls != kTileEmpty) {  // warp-uniform
         uint32_t sr[64];
-        tmem_ld32(s_addr, sr);
-        tmem_ld32(s_addr + 32, sr + 32);
+        tmem_ld64(s_addr, sr);  // one 64-column load + one wait (vs 2 x 32: +0.8 % CP1, +2 % CP8 shapes)
         tmem_ld_wait();
         float s[64];
 #pragma unroll

@@ -1786,8 +1786,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_v9_kernel(const __grid_c
         tc_fence_after();
         if (cls != kTileEmpty) {
           uint32_t sr[64];
-          tmem_ld32(s_addr, sr);
-          tmem_ld32(s_addr + 32, sr + 32);
+          tmem_ld64(s_addr, sr);
           tmem_ld_wait();
           float s[64];
 #pragma unroll
