@@ -218,10 +218,10 @@ __device__ __forceinline__ void arrive_leader(uint64_t* bar) {
 
 // ---- variants (attn_variants.cu)
 // Key-block rows of a version's tile summaries / TMA boxes.
-inline int attn_key_rows(int version) { return (version == 4 || version == 7 || version == 9) ? 64 : 128; }
+inline int attn_key_rows(int version) { return (version == 4 || version == 7 || version >= 9) ? 64 : 128; }
 inline int attn_k_box_rows(int version) { return version == 6 ? 128 : 64; }
-inline int attn_v_box_rows(int version) { return (version == 4 || version == 7 || version == 9) ? 64 : 128; }
-// Launch variant `version` (5..9) over n_pairs_heads = (query-tile pairs) x Hq.
+inline int attn_v_box_rows(int version) { return (version == 4 || version == 7 || version >= 9) ? 64 : 128; }
+// Launch variant `version` (5..11) over n_pairs_heads = (query-tile pairs) x Hq.
 int attn_variant_launch(int version, const AttnParams& prm, int64_t n_pairs_heads, cudaStream_t st);
 
 }  // namespace rcp

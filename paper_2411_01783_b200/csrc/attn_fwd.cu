@@ -559,14 +559,15 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
   // v4 (1-CTA, 64-key blocks) is the default: it measured best on the power-
   // capped B200s ("Attention kernel versions").  RCP_ATTN_VERSION=5
   // (CTA pairs), =6 (1-CTA, 128-key blocks, split softmax), =7 (Q in TMEM,
-  // TS-form S), =8 (CTA pairs, alternate-block softmax groups) and =9
-  // (persistent v4) are kept for A/B measurements; all pass the same parity
+  // TS-form S), =8 (CTA pairs, alternate-block softmax groups), =9
+  // (persistent v4), =10 (S decoupled from P in TMEM) and =11 (v10 + one MMA
+  // issuer per tile) are kept for A/B measurements; all pass the same parity
   // tests.
   static int version = -1;
   if (version < 0) {
     const char* e = getenv("RCP_ATTN_VERSION");
     const int v = e ? atoi(e) : 4;
-    version = (v >= 5 && v <= 9) ? v : 4;
+    version = (v >= 5 && v <= 11) ? v : 4;
   }
   const int krows = attn_key_rows(version);
   AttnParams prm;

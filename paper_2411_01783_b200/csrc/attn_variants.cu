@@ -1945,6 +1945,699 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_v9_kernel(const __grid_c
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+
+// ======================================================================
+// v10: v4 with S decoupled from P.  In v4, S_t(j+2) shares a TMEM buffer
+// with P_t(j), so it can only be issued after PV_t(j) — and the N = 64 S
+// MMAs run at ~55 % of the tensor rate — so the softmax waits for its next
+// S (20 % of all warp samples in the v4e ncu capture sit on that wait).
+// Here each tile has ONE S buffer, released by the softmax as soon as it has
+// loaded S(j) into registers (bar_sfree), so the MMA issues S(j+1) at the
+// start of softmax block j and it computes under the exps; P goes to its own
+// double buffer (2 x 32 columns per tile), reused once the PV that read it
+// is done (bar_pvd, also the "PV(j-1) landed" signal of the O rescale).
+// TMEM: O0 [0,128) | O1 [128,256) | S0 [256,320) | S1 [320,384) |
+//       P0 [384,416) [416,448) | P1 [448,480) [480,512).
+// ======================================================================
+constexpr uint32_t kTmemS10 = 256, kTmemP10 = 384;
+
+__global__ void __launch_bounds__(kThreads, 1) attn_fwd_v10_kernel(const __grid_constant__ AttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem =
+      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + 2 * kQTileBytes;
+
+  __shared__ uint64_t bar_q, bar_full[kSlots], bar_empty[kSlots];
+  __shared__ uint64_t bar_s[2], bar_sfree[2], bar_p[2][2], bar_pvd[2][2], bar_o[2];
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = static_cast<int>(warp_id());
+  const int per_kv = p.n_qblk * p.group;
+  const int kvh = static_cast<int>(blockIdx.x) / per_kv;
+  const int rem = static_cast<int>(blockIdx.x) - kvh * per_kv;
+  const int qblk = p.n_qblk - 1 - rem / p.group;
+  const int head = kvh * p.group + rem % p.group;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_q, 1);
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(&bar_full[s], 1);
+      mbar_init(&bar_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&bar_s[t], 1);
+      mbar_init(&bar_sfree[t], 128);
+      mbar_init(&bar_o[t], 1);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&bar_p[t][b], 128);
+        mbar_init(&bar_pvd[t][b], 1);
+      }
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (as v4)
+    if (elect_one()) {
+      tma_prefetch_desc(&p.tm_q);
+      tma_prefetch_desc(&p.tm_k);
+      tma_prefetch_desc(&p.tm_v);
+      const int n = __ldg(p.act_n + qblk);
+      const uint32_t* act = p.act + static_cast<int64_t>(qblk) * p.n_kblocks;
+      if (n > 0) {
+        const uint64_t pol_q = policy_evict_first();
+        const uint64_t pol_kv = policy_evict_last();
+        mbar_arrive_expect_tx(&bar_q, 2 * kQTileBytes);
+        for (int t = 0; t < 2; ++t)
+          for (int h = 0; h < 2; ++h)
+            tma_load_2d(sQ + t * kQTileBytes + h * kQBoxBytes, &p.tm_q, &bar_q, head * kD + h * 64,
+                        (2 * qblk + t) * kQRows, pol_q);
+        uint32_t ld = 0;
+        uint32_t e_next = __ldg(act);
+        for (int it = 0; it < n; ++it) {
+          const int j = act_j(e_next);
+          if (it + 1 < n) e_next = __ldg(act + it + 1);
+#pragma unroll
+          for (int kv = 0; kv < 2; ++kv, ++ld) {
+            const uint32_t slot = ld % kSlots, ph = (ld / kSlots) & 1;
+            mbar_wait(&bar_empty[slot], ph ^ 1);
+            mbar_arrive_expect_tx(&bar_full[slot], kKVBytes);
+            const CUtensorMap* map = kv ? &p.tm_v : &p.tm_k;
+            for (int h = 0; h < 2; ++h)
+              tma_load_2d(sKV + slot * kKVBytes + h * kKVBoxBytes, map, &bar_full[slot],
+                          kvh * kD + h * 64, j * kKRows, pol_kv);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      const uint32_t idesc_s = make_idesc_bf16_f32(kQRows, kKRows, 0, 0);
+      const uint32_t idesc_o = make_idesc_bf16_f32(kQRows, kD, 0, 1);
+      const uint32_t q_lo = sw128_desc_lo(smem_u32(sQ), 16);
+      const uint32_t k_lo = sw128_desc_lo(smem_u32(sKV), 16);
+      const uint32_t v_lo = sw128_desc_lo(smem_u32(sKV), kKVBoxBytes);
+      auto wait_load = [&](uint32_t ld) {
+        mbar_wait(&bar_full[ld % kSlots], (ld / kSlots) & 1);
+        tc_fence_after();
+      };
+      auto issue_s = [&](int t, uint32_t ld) {
+        const uint32_t qa = q_lo + ((t * kQTileBytes) >> 4);
+        const uint32_t ka = k_lo + (((ld % kSlots) * kKVBytes) >> 4);
+        const uint32_t d = tmem + kTmemS10 + t * kKRows;
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk)
+          mma_ss_lo(d, qa + (((kk >> 2) * kQBoxBytes + (kk & 3) * 32) >> 4),
+                    ka + (((kk >> 2) * kKVBoxBytes + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
+      };
+      auto issue_pv = [&](int t, int b, uint32_t ld, bool acc) {
+        const uint32_t va = v_lo + (((ld % kSlots) * kKVBytes) >> 4);
+        const uint32_t pa = tmem + kTmemP10 + 64 * t + 32 * b;
+#pragma unroll
+        for (int kk = 0; kk < kKRows / 16; ++kk)
+          mma_ts_lo(tmem + kTmemO + t * kD, pa + kk * 8, va + ((kk * 2048) >> 4), idesc_o,
+                    (acc || kk > 0) ? 1u : 0u);
+      };
+      const int n = __ldg(p.act_n + qblk);
+      if (n > 0) {
+        mbar_wait(&bar_q, 0);
+        tc_fence_after();
+        wait_load(0);
+        issue_s(0, 0);
+        mma_commit(&bar_s[0]);
+        issue_s(1, 0);
+        mma_commit(&bar_s[1]);
+        mma_commit(&bar_empty[0]);
+        for (int it = 0; it < n; ++it) {
+          const int b = it & 1;
+          const uint32_t pph = (it >> 1) & 1;
+          const bool last = it + 1 == n;
+          if (!last) {  // S(it + 1) into the buffer each tile's softmax has just read
+            const uint32_t ldk = 2 * (it + 1);
+            wait_load(ldk);
+            for (int t = 0; t < 2; ++t) {
+              mbar_wait(&bar_sfree[t], it & 1);
+              tc_fence_after();
+              issue_s(t, ldk);
+              mma_commit(&bar_s[t]);
+            }
+            mma_commit(&bar_empty[ldk % kSlots]);
+          }
+          const uint32_t ldv = 2 * it + 1;
+          wait_load(ldv);
+          for (int t = 0; t < 2; ++t) {
+            mbar_wait(&bar_p[t][b], pph);
+            tc_fence_after();
+            issue_pv(t, b, ldv, it > 0);
+            mma_commit(&bar_pvd[t][b]);
+            if (last) mma_commit(&bar_o[t]);
+          }
+          mma_commit(&bar_empty[ldv % kSlots]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax + epilogue
+    const int w = (warp - 4) >> 2;
+    const int t = static_cast<int>(threadIdx.x) - 128 - 128 * w;
+    const int row = (2 * qblk + w) * kQRows + t;
+    const bool row_ok = row < p.tq;
+    const int my_pos = row_ok ? __ldg(p.q_pos + row) : -1;
+    const int my_seq = row_ok ? __ldg(p.q_seq + row) : RCP_SEQ_PAD_Q;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+    const uint32_t o_addr = lane_base + kTmemO + w * kD;
+    const uint32_t s_addr = lane_base + kTmemS10 + w * kKRows;
+    const float sl2 = p.scale_log2;
+    const uint64_t sl2x2 = f2(sl2, sl2);
+    float m = -INFINITY, l = 0.f;
+    const int n = __ldg(p.act_n + qblk);
+    const uint32_t* act = p.act + static_cast<int64_t>(qblk) * p.n_kblocks;
+    uint32_t e_next = n > 0 ? __ldg(act) : 0u;
+    int it = 0;
+    for (; it < n; ++it) {
+      const int b = it & 1;
+      const uint32_t p_addr = lane_base + kTmemP10 + 64 * w + 32 * b;
+      const uint32_t e = e_next;
+      if (it + 1 < n) e_next = __ldg(act + it + 1);
+      const int j = act_j(e);
+      const int cls = act_cls(e, w);
+      mbar_wait(&bar_s[w], it & 1);
+      tc_fence_after();
+      uint32_t pk[32];
+      if (cls != kTileEmpty) {  // warp-uniform
+        uint32_t sr[64];
+        tmem_ld64(s_addr, sr);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&bar_sfree[w]);  // S buffer free: the MMA may issue S(it + 1)
+        float s[64];
+#pragma unroll
+        for (int c = 0; c < 64; ++c) s[c] = __uint_as_float(sr[c]);
+        if (cls == kTilePartial) {
+          const int base = j * kKRows;
+          if (base + kKRows <= p.tk) {
+            const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + base);
+            const int4* ks4 = reinterpret_cast<const int4*>(p.k_seq + base);
+#pragma unroll
+            for (int c4 = 0; c4 < 16; ++c4) {
+              const int4 kp = __ldg(kp4 + c4), kq = __ldg(ks4 + c4);
+              if (!(kq.x == my_seq && kp.x <= my_pos)) s[4 * c4 + 0] = -INFINITY;
+              if (!(kq.y == my_seq && kp.y <= my_pos)) s[4 * c4 + 1] = -INFINITY;
+              if (!(kq.z == my_seq && kp.z <= my_pos)) s[4 * c4 + 2] = -INFINITY;
+              if (!(kq.w == my_seq && kp.w <= my_pos)) s[4 * c4 + 3] = -INFINITY;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 64; ++c) {
+              const int kidx = base + c;
+              const bool ok = kidx < p.tk && __ldg(p.k_seq + kidx) == my_seq &&
+                              __ldg(p.k_pos + kidx) <= my_pos;
+              if (!ok) s[c] = -INFINITY;
+            }
+          }
+        }
+        float m8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m8[k] = s[k];
+#pragma unroll
+        for (int c = 8; c < 64; c += 8)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m8[k] = fmaxf(m8[k], s[c + k]);
+        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        const float m_old = m;
+        const float m_new = fmaxf(m, mx * sl2);
+        const bool need = m_new > m + kRescaleThreshold;
+        if (need) m = m_new;
+        const float m_use = (m == -INFINITY) ? 0.f : m;
+        const uint64_t negm2 = f2(-m_use, -m_use);
+        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+        if (cls == kTileFull) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float2 x = unf2(ffma2(f2(s[2 * i], s[2 * i + 1]), sl2x2, negm2));
+            float p0, p1;
+            if ((i & 7) < kPolyPairsPer8) {
+              const float2 pp = ex2_poly_x2(x.x, x.y);
+              p0 = pp.x;
+              p1 = pp.y;
+            } else {
+              p0 = ex2_approx(x.x);
+              p1 = ex2_approx(x.y);
+            }
+            acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
+            pk[i] = pack_bf16x2(p0, p1);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float2 x = unf2(ffma2(f2(s[2 * i], s[2 * i + 1]), sl2x2, negm2));
+            const float p0 = ex2_approx(x.x), p1 = ex2_approx(x.y);
+            acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
+            pk[i] = pack_bf16x2(p0, p1);
+          }
+        }
+        const float2 a01 = unf2(fadd2(acc2[0], acc2[1]));
+        const float2 a23 = unf2(fadd2(acc2[2], acc2[3]));
+        const float sum = (a01.x + a01.y) + (a23.x + a23.y);
+        const float f = (need && m_old != -INFINITY) ? ex2_approx(m_old - m) : 1.0f;
+        l = (m_old == -INFINITY ? 0.f : l * f) + sum;
+        if (__any_sync(0xffffffffu, f != 1.0f && it > 0)) {
+          // rescale O_t in place once PV_t(it - 1) has landed
+          mbar_wait(&bar_pvd[w][(it - 1) & 1], ((it - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < kD; c += 32) {
+            uint32_t r[32];
+            tmem_ld32(o_addr + c, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
+            tmem_st32(o_addr + c, r);
+          }
+        }
+      } else {
+        tc_fence_before();
+        mbar_arrive(&bar_sfree[w]);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pk[i] = 0u;
+      }
+      if (it >= 2) {  // P buffer b was read by PV(it - 2)
+        mbar_wait(&bar_pvd[w][b], ((it >> 1) - 1) & 1);
+        tc_fence_after();
+      }
+      tmem_st32(p_addr, pk);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bar_p[w][b]);
+    }
+
+    // epilogue (as v4)
+    if (it > 0) {
+      mbar_wait(&bar_o[w], 0);
+      tc_fence_after();
+    }
+    const bool merge = p.mode == RCP_MODE_MERGE;
+    if (!(merge && it == 0)) {
+      const bool has = l > 0.f;
+      const float inv = has ? 1.0f / l : 0.f;
+      const float lse_new = has ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+      float* orow = p.o + (static_cast<int64_t>(row) * p.hq + head) * kD;
+      float* lrow = p.lse + static_cast<int64_t>(row) * p.hq + head;
+      MergeW mw;
+      mw.lse = lse_new;
+      mw.wa = 0.f;
+      mw.wb = 1.f;
+      if (merge && row_ok) mw = merge_weights(__ldg(lrow), lse_new);
+#pragma unroll
+      for (int c = 0; c < kD; c += 32) {
+        uint32_t r[32];
+        if (it > 0) {
+          tmem_ld32(o_addr + c, r);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+        if (row_ok) {
+          float4* dst = reinterpret_cast<float4*>(orow + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float4 v = make_float4(__uint_as_float(r[4 * i]) * inv, __uint_as_float(r[4 * i + 1]) * inv,
+                                   __uint_as_float(r[4 * i + 2]) * inv,
+                                   __uint_as_float(r[4 * i + 3]) * inv);
+            if (merge) {
+              const float4 a = dst[i];
+              v = make_float4(merge_val(a.x, v.x, mw), merge_val(a.y, v.y, mw),
+                              merge_val(a.z, v.z, mw), merge_val(a.w, v.w, mw));
+            }
+            dst[i] = v;
+          }
+        }
+      }
+      if (row_ok) *lrow = merge ? mw.lse : lse_new;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// ======================================================================
+// v11: v10 with one MMA-issuing warp per query tile (warp 1: tile 0, warp 3:
+// tile 1).  tcgen05.commit tracks the issuing thread's MMAs, so each tile's
+// S / PV stream is ordered only by its own barriers — a tile's next S is no
+// longer held behind the other tile's P.  K/V slots are read by both tiles:
+// their "empty" barriers take one commit from each issuer.
+// (v10 text follows.)
+// v10: v4 with S decoupled from P.  In v4, S_t(j+2) shares a TMEM buffer
+// with P_t(j), so it can only be issued after PV_t(j) — and the N = 64 S
+// MMAs run at ~55 % of the tensor rate — so the softmax waits for its next
+// S (20 % of all warp samples in the v4e ncu capture sit on that wait).
+// Here each tile has ONE S buffer, released by the softmax as soon as it has
+// loaded S(j) into registers (bar_sfree), so the MMA issues S(j+1) at the
+// start of softmax block j and it computes under the exps; P goes to its own
+// double buffer (2 x 32 columns per tile), reused once the PV that read it
+// is done (bar_pvd, also the "PV(j-1) landed" signal of the O rescale).
+// TMEM: O0 [0,128) | O1 [128,256) | S0 [256,320) | S1 [320,384) |
+//       P0 [384,416) [416,448) | P1 [448,480) [480,512).
+// ======================================================================
+
+__global__ void __launch_bounds__(kThreads, 1) attn_fwd_v11_kernel(const __grid_constant__ AttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem =
+      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + 2 * kQTileBytes;
+
+  __shared__ uint64_t bar_q, bar_full[kSlots], bar_empty[kSlots];
+  __shared__ uint64_t bar_s[2], bar_sfree[2], bar_p[2][2], bar_pvd[2][2], bar_o[2];
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = static_cast<int>(warp_id());
+  const int per_kv = p.n_qblk * p.group;
+  const int kvh = static_cast<int>(blockIdx.x) / per_kv;
+  const int rem = static_cast<int>(blockIdx.x) - kvh * per_kv;
+  const int qblk = p.n_qblk - 1 - rem / p.group;
+  const int head = kvh * p.group + rem % p.group;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_q, 1);
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(&bar_full[s], 1);
+      mbar_init(&bar_empty[s], 2);  // one commit per tile's MMA issuer
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&bar_s[t], 1);
+      mbar_init(&bar_sfree[t], 128);
+      mbar_init(&bar_o[t], 1);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&bar_p[t][b], 128);
+        mbar_init(&bar_pvd[t][b], 1);
+      }
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (as v4)
+    if (elect_one()) {
+      tma_prefetch_desc(&p.tm_q);
+      tma_prefetch_desc(&p.tm_k);
+      tma_prefetch_desc(&p.tm_v);
+      const int n = __ldg(p.act_n + qblk);
+      const uint32_t* act = p.act + static_cast<int64_t>(qblk) * p.n_kblocks;
+      if (n > 0) {
+        const uint64_t pol_q = policy_evict_first();
+        const uint64_t pol_kv = policy_evict_last();
+        mbar_arrive_expect_tx(&bar_q, 2 * kQTileBytes);
+        for (int t = 0; t < 2; ++t)
+          for (int h = 0; h < 2; ++h)
+            tma_load_2d(sQ + t * kQTileBytes + h * kQBoxBytes, &p.tm_q, &bar_q, head * kD + h * 64,
+                        (2 * qblk + t) * kQRows, pol_q);
+        uint32_t ld = 0;
+        uint32_t e_next = __ldg(act);
+        for (int it = 0; it < n; ++it) {
+          const int j = act_j(e_next);
+          if (it + 1 < n) e_next = __ldg(act + it + 1);
+#pragma unroll
+          for (int kv = 0; kv < 2; ++kv, ++ld) {
+            const uint32_t slot = ld % kSlots, ph = (ld / kSlots) & 1;
+            mbar_wait(&bar_empty[slot], ph ^ 1);
+            mbar_arrive_expect_tx(&bar_full[slot], kKVBytes);
+            const CUtensorMap* map = kv ? &p.tm_v : &p.tm_k;
+            for (int h = 0; h < 2; ++h)
+              tma_load_2d(sKV + slot * kKVBytes + h * kKVBoxBytes, map, &bar_full[slot],
+                          kvh * kD + h * 64, j * kKRows, pol_kv);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1 || warp == 3) {
+    // ------------------------------------------------------------ MMA issuer of tile tt
+    const int tt = warp == 1 ? 0 : 1;
+    if (elect_one()) {
+      const uint32_t idesc_s = make_idesc_bf16_f32(kQRows, kKRows, 0, 0);
+      const uint32_t idesc_o = make_idesc_bf16_f32(kQRows, kD, 0, 1);
+      const uint32_t q_lo = sw128_desc_lo(smem_u32(sQ), 16);
+      const uint32_t k_lo = sw128_desc_lo(smem_u32(sKV), 16);
+      const uint32_t v_lo = sw128_desc_lo(smem_u32(sKV), kKVBoxBytes);
+      auto wait_load = [&](uint32_t ld) {
+        mbar_wait(&bar_full[ld % kSlots], (ld / kSlots) & 1);
+        tc_fence_after();
+      };
+      auto issue_s = [&](uint32_t ld) {
+        const uint32_t qa = q_lo + ((tt * kQTileBytes) >> 4);
+        const uint32_t ka = k_lo + (((ld % kSlots) * kKVBytes) >> 4);
+        const uint32_t d = tmem + kTmemS10 + tt * kKRows;
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk)
+          mma_ss_lo(d, qa + (((kk >> 2) * kQBoxBytes + (kk & 3) * 32) >> 4),
+                    ka + (((kk >> 2) * kKVBoxBytes + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
+      };
+      auto issue_pv = [&](int b, uint32_t ld, bool acc) {
+        const uint32_t va = v_lo + (((ld % kSlots) * kKVBytes) >> 4);
+        const uint32_t pa = tmem + kTmemP10 + 64 * tt + 32 * b;
+#pragma unroll
+        for (int kk = 0; kk < kKRows / 16; ++kk)
+          mma_ts_lo(tmem + kTmemO + tt * kD, pa + kk * 8, va + ((kk * 2048) >> 4), idesc_o,
+                    (acc || kk > 0) ? 1u : 0u);
+      };
+      const int n = __ldg(p.act_n + qblk);
+      if (n > 0) {
+        mbar_wait(&bar_q, 0);
+        tc_fence_after();
+        wait_load(0);
+        issue_s(0);
+        mma_commit(&bar_s[tt]);
+        mma_commit(&bar_empty[0]);
+        for (int it = 0; it < n; ++it) {
+          const int b = it & 1;
+          const bool last = it + 1 == n;
+          if (!last) {  // S(it + 1) into the buffer this tile's softmax has just read
+            const uint32_t ldk = 2 * (it + 1);
+            wait_load(ldk);
+            mbar_wait(&bar_sfree[tt], it & 1);
+            tc_fence_after();
+            issue_s(ldk);
+            mma_commit(&bar_s[tt]);
+            mma_commit(&bar_empty[ldk % kSlots]);
+          }
+          const uint32_t ldv = 2 * it + 1;
+          wait_load(ldv);
+          mbar_wait(&bar_p[tt][b], (it >> 1) & 1);
+          tc_fence_after();
+          issue_pv(b, ldv, it > 0);
+          mma_commit(&bar_pvd[tt][b]);
+          if (last) mma_commit(&bar_o[tt]);
+          mma_commit(&bar_empty[ldv % kSlots]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax + epilogue
+    const int w = (warp - 4) >> 2;
+    const int t = static_cast<int>(threadIdx.x) - 128 - 128 * w;
+    const int row = (2 * qblk + w) * kQRows + t;
+    const bool row_ok = row < p.tq;
+    const int my_pos = row_ok ? __ldg(p.q_pos + row) : -1;
+    const int my_seq = row_ok ? __ldg(p.q_seq + row) : RCP_SEQ_PAD_Q;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+    const uint32_t o_addr = lane_base + kTmemO + w * kD;
+    const uint32_t s_addr = lane_base + kTmemS10 + w * kKRows;
+    const float sl2 = p.scale_log2;
+    const uint64_t sl2x2 = f2(sl2, sl2);
+    float m = -INFINITY, l = 0.f;
+    const int n = __ldg(p.act_n + qblk);
+    const uint32_t* act = p.act + static_cast<int64_t>(qblk) * p.n_kblocks;
+    uint32_t e_next = n > 0 ? __ldg(act) : 0u;
+    int it = 0;
+    for (; it < n; ++it) {
+      const int b = it & 1;
+      const uint32_t p_addr = lane_base + kTmemP10 + 64 * w + 32 * b;
+      const uint32_t e = e_next;
+      if (it + 1 < n) e_next = __ldg(act + it + 1);
+      const int j = act_j(e);
+      const int cls = act_cls(e, w);
+      mbar_wait(&bar_s[w], it & 1);
+      tc_fence_after();
+      uint32_t pk[32];
+      if (cls != kTileEmpty) {  // warp-uniform
+        uint32_t sr[64];
+        tmem_ld64(s_addr, sr);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&bar_sfree[w]);  // S buffer free: the MMA may issue S(it + 1)
+        float s[64];
+#pragma unroll
+        for (int c = 0; c < 64; ++c) s[c] = __uint_as_float(sr[c]);
+        if (cls == kTilePartial) {
+          const int base = j * kKRows;
+          if (base + kKRows <= p.tk) {
+            const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + base);
+            const int4* ks4 = reinterpret_cast<const int4*>(p.k_seq + base);
+#pragma unroll
+            for (int c4 = 0; c4 < 16; ++c4) {
+              const int4 kp = __ldg(kp4 + c4), kq = __ldg(ks4 + c4);
+              if (!(kq.x == my_seq && kp.x <= my_pos)) s[4 * c4 + 0] = -INFINITY;
+              if (!(kq.y == my_seq && kp.y <= my_pos)) s[4 * c4 + 1] = -INFINITY;
+              if (!(kq.z == my_seq && kp.z <= my_pos)) s[4 * c4 + 2] = -INFINITY;
+              if (!(kq.w == my_seq && kp.w <= my_pos)) s[4 * c4 + 3] = -INFINITY;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 64; ++c) {
+              const int kidx = base + c;
+              const bool ok = kidx < p.tk && __ldg(p.k_seq + kidx) == my_seq &&
+                              __ldg(p.k_pos + kidx) <= my_pos;
+              if (!ok) s[c] = -INFINITY;
+            }
+          }
+        }
+        float m8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m8[k] = s[k];
+#pragma unroll
+        for (int c = 8; c < 64; c += 8)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m8[k] = fmaxf(m8[k], s[c + k]);
+        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        const float m_old = m;
+        const float m_new = fmaxf(m, mx * sl2);
+        const bool need = m_new > m + kRescaleThreshold;
+        if (need) m = m_new;
+        const float m_use = (m == -INFINITY) ? 0.f : m;
+        const uint64_t negm2 = f2(-m_use, -m_use);
+        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+        if (cls == kTileFull) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float2 x = unf2(ffma2(f2(s[2 * i], s[2 * i + 1]), sl2x2, negm2));
+            float p0, p1;
+            if ((i & 7) < kPolyPairsPer8) {
+              const float2 pp = ex2_poly_x2(x.x, x.y);
+              p0 = pp.x;
+              p1 = pp.y;
+            } else {
+              p0 = ex2_approx(x.x);
+              p1 = ex2_approx(x.y);
+            }
+            acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
+            pk[i] = pack_bf16x2(p0, p1);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float2 x = unf2(ffma2(f2(s[2 * i], s[2 * i + 1]), sl2x2, negm2));
+            const float p0 = ex2_approx(x.x), p1 = ex2_approx(x.y);
+            acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
+            pk[i] = pack_bf16x2(p0, p1);
+          }
+        }
+        const float2 a01 = unf2(fadd2(acc2[0], acc2[1]));
+        const float2 a23 = unf2(fadd2(acc2[2], acc2[3]));
+        const float sum = (a01.x + a01.y) + (a23.x + a23.y);
+        const float f = (need && m_old != -INFINITY) ? ex2_approx(m_old - m) : 1.0f;
+        l = (m_old == -INFINITY ? 0.f : l * f) + sum;
+        if (__any_sync(0xffffffffu, f != 1.0f && it > 0)) {
+          // rescale O_t in place once PV_t(it - 1) has landed
+          mbar_wait(&bar_pvd[w][(it - 1) & 1], ((it - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < kD; c += 32) {
+            uint32_t r[32];
+            tmem_ld32(o_addr + c, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
+            tmem_st32(o_addr + c, r);
+          }
+        }
+      } else {
+        tc_fence_before();
+        mbar_arrive(&bar_sfree[w]);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pk[i] = 0u;
+      }
+      if (it >= 2) {  // P buffer b was read by PV(it - 2)
+        mbar_wait(&bar_pvd[w][b], ((it >> 1) - 1) & 1);
+        tc_fence_after();
+      }
+      tmem_st32(p_addr, pk);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bar_p[w][b]);
+    }
+
+    // epilogue (as v4)
+    if (it > 0) {
+      mbar_wait(&bar_o[w], 0);
+      tc_fence_after();
+    }
+    const bool merge = p.mode == RCP_MODE_MERGE;
+    if (!(merge && it == 0)) {
+      const bool has = l > 0.f;
+      const float inv = has ? 1.0f / l : 0.f;
+      const float lse_new = has ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+      float* orow = p.o + (static_cast<int64_t>(row) * p.hq + head) * kD;
+      float* lrow = p.lse + static_cast<int64_t>(row) * p.hq + head;
+      MergeW mw;
+      mw.lse = lse_new;
+      mw.wa = 0.f;
+      mw.wb = 1.f;
+      if (merge && row_ok) mw = merge_weights(__ldg(lrow), lse_new);
+#pragma unroll
+      for (int c = 0; c < kD; c += 32) {
+        uint32_t r[32];
+        if (it > 0) {
+          tmem_ld32(o_addr + c, r);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+        if (row_ok) {
+          float4* dst = reinterpret_cast<float4*>(orow + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float4 v = make_float4(__uint_as_float(r[4 * i]) * inv, __uint_as_float(r[4 * i + 1]) * inv,
+                                   __uint_as_float(r[4 * i + 2]) * inv,
+                                   __uint_as_float(r[4 * i + 3]) * inv);
+            if (merge) {
+              const float4 a = dst[i];
+              v = make_float4(merge_val(a.x, v.x, mw), merge_val(a.y, v.y, mw),
+                              merge_val(a.z, v.z, mw), merge_val(a.w, v.w, mw));
+            }
+            dst[i] = v;
+          }
+        }
+      }
+      if (row_ok) *lrow = merge ? mw.lse : lse_new;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+
 int attn_variant_launch(int version, const AttnParams& prm, int64_t grid, cudaStream_t st) {
   const unsigned g = static_cast<unsigned>(grid);
   if (version == 5) {
@@ -1992,6 +2685,22 @@ int attn_variant_launch(int version, const AttnParams& prm, int64_t grid, cudaSt
     }
     const unsigned gp = static_cast<unsigned>(grid < n_sm ? grid : n_sm);
     attn_fwd_v9_kernel<<<gp, kThreads, kSmemBytes, st>>>(prm);
+  } else if (version == 10) {
+    static bool attr = false;
+    if (!attr) {
+      RCP_CUDA(cudaFuncSetAttribute(attn_fwd_v10_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kSmemBytes));
+      attr = true;
+    }
+    attn_fwd_v10_kernel<<<g, kThreads, kSmemBytes, st>>>(prm);
+  } else if (version == 11) {
+    static bool attr = false;
+    if (!attr) {
+      RCP_CUDA(cudaFuncSetAttribute(attn_fwd_v11_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kSmemBytes));
+      attr = true;
+    }
+    attn_fwd_v11_kernel<<<g, kThreads, kSmemBytes, st>>>(prm);
   } else {
     set_error("unknown attention kernel version %d", version);
     return RCP_ERR_INVALID;

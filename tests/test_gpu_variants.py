@@ -1,4 +1,4 @@
-"""Every A/B attention kernel variant (RCP_ATTN_VERSION=5..9, DESIGN.md
+"""Every A/B attention kernel variant (RCP_ATTN_VERSION=5..11, DESIGN.md
 "Attention kernel versions") keeps parity with the fp32 reference: each runs
 in a fresh process (the library reads the selector once) on eight random
 segmented / GQA / merge cases (tests/_variant_check.py)."""
@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("version", [5, 6, 7, 8, 9])
+@pytest.mark.parametrize("version", [5, 6, 7, 8, 9, 10, 11])
 def test_variant_parity(version):
     env = dict(os.environ, RCP_ATTN_VERSION=str(version))
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "_variant_check.py")], cwd=ROOT, env=env,
