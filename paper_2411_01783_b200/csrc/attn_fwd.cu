@@ -6,7 +6,8 @@
 //
 // Warp roles (384 threads):
 //   warp 0      TMA producer (one elected lane): Q once, then K_j / V_j
-//   warp 1      MMA issuer (one elected lane):   S_t(j) = Q_t K_j^T   (SS, K-major)
+//   warps 1, 3  MMA issuers of tiles 0 / 1 (one elected lane each):
+//                                                S_t(j) = Q_t K_j^T   (SS, K-major)
 //                                                O_t   += P_t(j) V_j  (TS, P in TMEM)
 //   warp 2      TMEM allocator
 //   warps 4-7   softmax for query tile 0 (thread i owns TMEM lane / row i)
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     mbar_init(&bar_q, 1);
     for (int s = 0; s < kSlots; ++s) {
       mbar_init(&bar_full[s], 1);
-      mbar_init(&bar_empty[s], 1);
+      mbar_init(&bar_empty[s], 2);  // one commit per tile's MMA issuer
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&bar_s[t][0], 1);
@@ -182,8 +183,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (one elected lane)
+  } else if (warp == 1 || warp == 3) {
+    // ------------------------------------------------------------ MMA issuers: warp 1 tile 0, warp 3 tile 1
+    // Each tile's PV(j), S(j+2) stream is ordered only by its own P barriers,
+    // so one tile's next S is never held behind the other tile's P (a single
+    // issuer measured 2-3.5 % slower).  tcgen05.commit tracks the issuing
+    // thread's MMAs; K/V slots, read by both tiles, take one commit from each.
+    const int tt = warp == 1 ? 0 : 1;
     if (elect_one()) {
       const uint32_t idesc_s = make_idesc_bf16_f32(kQRows, kKRows, 0, 0);
       const uint32_t idesc_o = make_idesc_bf16_f32(kQRows, kD, 0, 1);
@@ -195,39 +201,35 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         mbar_wait(&bar_full[ld % kSlots], (ld / kSlots) & 1);
         tc_fence_after();
       };
-      auto issue_s = [&](int t, int buf, uint32_t ld) {
-        const uint32_t qa = q_lo + ((t * kQTileBytes) >> 4);
+      auto issue_s = [&](int buf, uint32_t ld) {
+        const uint32_t qa = q_lo + ((tt * kQTileBytes) >> 4);
         const uint32_t ka = k_lo + (((ld % kSlots) * kKVBytes) >> 4);
-        const uint32_t d = tmem + kTmemS + (2 * t + buf) * kKRows;
+        const uint32_t d = tmem + kTmemS + (2 * tt + buf) * kKRows;
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk)
           mma_ss_lo(d, qa + (((kk >> 2) * kQBoxBytes + (kk & 3) * 32) >> 4),
                     ka + (((kk >> 2) * kKVBoxBytes + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
       };
-      auto issue_pv = [&](int t, int buf, uint32_t ld, bool acc) {
+      auto issue_pv = [&](int buf, uint32_t ld, bool acc) {
         const uint32_t va = v_lo + (((ld % kSlots) * kKVBytes) >> 4);
-        const uint32_t pa = tmem + kTmemS + (2 * t + buf) * kKRows;
+        const uint32_t pa = tmem + kTmemS + (2 * tt + buf) * kKRows;
 #pragma unroll
         for (int kk = 0; kk < kKRows / 16; ++kk)
-          mma_ts_lo(tmem + kTmemO + t * kD, pa + kk * 8, va + ((kk * 2048) >> 4), idesc_o,
+          mma_ts_lo(tmem + kTmemO + tt * kD, pa + kk * 8, va + ((kk * 2048) >> 4), idesc_o,
                     (acc || kk > 0) ? 1u : 0u);
       };
       const int n = __ldg(p.act_n + qblk);
       if (n > 0) {
         mbar_wait(&bar_q, 0);
-        // prologue: S(0) and S(1) for both tiles
+        // prologue: S(0) and S(1) of this tile
         wait_load(0);
-        issue_s(0, 0, 0);
-        mma_commit(&bar_s[0][0]);
-        issue_s(1, 0, 0);
-        mma_commit(&bar_s[1][0]);
+        issue_s(0, 0);
+        mma_commit(&bar_s[tt][0]);
         mma_commit(&bar_empty[0]);
         if (n > 1) {
           wait_load(2);
-          issue_s(0, 1, 2);
-          mma_commit(&bar_s[0][1]);
-          issue_s(1, 1, 2);
-          mma_commit(&bar_s[1][1]);
+          issue_s(1, 2);
+          mma_commit(&bar_s[tt][1]);
           mma_commit(&bar_empty[2 % kSlots]);
         }
         for (int it = 0; it < n; ++it) {
@@ -235,32 +237,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
           const bool last = it + 1 == n, has2 = it + 2 < n;
           const uint32_t ldv = 2 * it + 1, ldk2 = 2 * it + 4;
           wait_load(ldv);
-          TRACE(12, it);
-          // tile 0: PV0(it) then, into the same buffer, S0(it+2)
-          mbar_wait(&bar_p[0][buf], (it >> 1) & 1);
+          if (tt == 0) TRACE(12, it);
+          // PV(it), then into the same buffer S(it+2) (tcgen05 ops complete in issue order)
+          mbar_wait(&bar_p[tt][buf], (it >> 1) & 1);
           tc_fence_after();
-          TRACE(0, it);
-          issue_pv(0, buf, ldv, it > 0);
-          mma_commit(last ? &bar_o[0] : &bar_pv[0]);
+          TRACE(tt, it);
+          issue_pv(buf, ldv, it > 0);
+          mma_commit(last ? &bar_o[tt] : &bar_pv[tt]);
+          mma_commit(&bar_empty[ldv % kSlots]);
+          if (tt == 1) TRACE(13, it);
           if (has2) {
             wait_load(ldk2);
-            issue_s(0, buf, ldk2);
-            mma_commit(&bar_s[0][buf]);
-          }
-          // tile 1
-          mbar_wait(&bar_p[1][buf], (it >> 1) & 1);
-          tc_fence_after();
-          TRACE(1, it);
-          issue_pv(1, buf, ldv, it > 0);
-          mma_commit(last ? &bar_o[1] : &bar_pv[1]);
-          mma_commit(&bar_empty[ldv % kSlots]);
-          TRACE(13, it);
-          if (has2) {
-            issue_s(1, buf, ldk2);
-            mma_commit(&bar_s[1][buf]);
+            issue_s(buf, ldk2);
+            mma_commit(&bar_s[tt][buf]);
             mma_commit(&bar_empty[ldk2 % kSlots]);
           }
-          TRACE(14, it);
+          if (tt == 1) TRACE(14, it);
         }
       }
     }

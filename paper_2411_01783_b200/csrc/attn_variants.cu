@@ -2638,6 +2638,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_v11_kernel(const __grid_
 }
 
 
+
 int attn_variant_launch(int version, const AttnParams& prm, int64_t grid, cudaStream_t st) {
   const unsigned g = static_cast<unsigned>(grid);
   if (version == 5) {
