@@ -304,6 +304,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     barrier()
+    last = None
     n0 = _lib.launch_count
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
@@ -312,7 +313,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         barrier()
         t0.record()
         for _ in range(args.steps):
-            step()
+            last = step()
         t1.record()
         barrier()
     timing["on"] = False
@@ -324,6 +325,26 @@ def run_ours(args, cfg, rank, world, local_rank):
     per_launch_flops = flops_rank / world  # world ring steps per call
     achieved = per_launch_flops / (attn_avg_ms * 1e-3) / 1e12
     attn_share = sum(attn_ms) / (ms_rank * args.steps)
+
+    # ---------------- parity of the timed output (outside the timed region):
+    # sampled query rows of the LAST timed step vs the fp64 oracle
+    parity = None
+    if args.check:
+        from oracle.sampled_check import check_rank_rows
+
+        rows_n = args.check_rows or {"8b": 32, "405b": 16, "405b-1m": 4}[args.config]
+        res = check_rank_rows(T, world, rank, last.output.data, last.lse, tens["q"], tens["k"], tens["v"],
+                              hkv, gcfg.scale, count=rows_n)
+        agg = torch.tensor([res["max_dO"], res["max_dLSE"], float(res["rows"])], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(agg[:2], op=dist.ReduceOp.MAX)
+            dist.all_reduce(agg[2:], op=dist.ReduceOp.SUM)
+        d_o, d_l, nrows = (float(x) for x in agg.cpu())
+        parity = {"rows": int(nrows), "heads": hq, "max_dO": d_o, "max_dLSE": d_l,
+                  "tol": {"dO": 2e-2, "dLSE": 1e-3}, "pass": d_o <= 2e-2 and d_l <= 1e-3,
+                  "oracle": "fp64 gqa_attention over 16K-key blocks + merge_attention (oracle/sampled_check.py)",
+                  "rows_from": "first/last token, both sides of every 2N-chunk boundary, random"}
+    del last
 
     # ---------------- exposed communication: the same kernels on the same per-step
     # KV blocks (all-gathered once beforehand), with the ring transfers removed
@@ -423,6 +444,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "launch_ms": attn_avg_ms, "flops_per_launch": per_launch_flops,
                      "attn_share_of_step": attn_share},
         "cpu_baseline": cpu,
+        "parity": parity,
         "e2e": e2e,
         "exposed_comm": exposed,
         "gpu_launches": launches,
@@ -442,10 +464,17 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=8)
+    ap.add_argument("--check", action="store_true",
+                    help="after timing, check sampled rows of the last timed output against the fp64 oracle")
+    ap.add_argument("--check-rows", type=int, default=None)
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.seq_len:
         cfg["T"] = args.seq_len
+        model = "llama3-8b" if args.config == "8b" else "llama3-405b"
+        T = args.seq_len
+        tok = f"{T >> 20}m" if T % (1 << 20) == 0 else (f"{T >> 10}k" if T % 1024 == 0 else str(T))
+        cfg["workload"] = f"{model}-attn-{tok}-full-prefill-pass-kv"
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

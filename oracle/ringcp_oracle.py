@@ -450,3 +450,85 @@ def comm_bytes(new_len, cached_len, model_dim, n_q, n_kv, elem_bytes, kind) -> f
     if kind == "Q":
         return float(new_len * model_dim * elem_bytes)
     return 2.0 * (new_len + cached_len) * model_dim * (n_kv / n_q) * elem_bytes
+
+
+# --------------------------------------------------------------------------- large-T (sampled rows)
+def gqa_grouped(q: Blk, k: Blk, v: Blk, n_kv_heads: int, scale: float | None = None):
+    """gqa_attention (attention.py:230-282) evaluated per KV-head group with
+    fp64 matrix products instead of the [H, Tq, Tk] einsum, so a few query
+    rows against 10^5-10^6 keys run on BLAS.  Same semantics as ``gqa``:
+    padding keys dropped first (attention.py:253-255), mask = _admissible
+    (attention.py:199-206), row max / exp / sum / PV in fp64, natural-log LSE,
+    zero / -inf rows without keys.  Agrees with ``gqa`` to ~1e-15 (summation
+    order differs); pinned by tests/test_oracle_sampled.py."""
+    tq, hq, d = q.data.shape
+    if scale is None:
+        scale = default_scale(d)
+    out = np.zeros((tq, hq, d), np.float64)
+    lse = np.full((tq, hq), NEG_INF, np.float64)
+    keep = k.valid
+    if tq == 0 or not keep.any():
+        return out, lse
+    kpos, kseq = k.pos[keep], k.seq[keep]
+    adm = admit_mask(q.valid, q.pos, q.seq, np.ones(kpos.size, bool), kpos, kseq)  # [Tq, Tk]
+    if not adm.any():
+        return out, lse
+    heads_of = kv_head_of(hq, n_kv_heads)
+    for g in range(n_kv_heads):
+        hs = np.flatnonzero(heads_of == g)
+        kg = k.data[keep][:, g, :].astype(np.float64)            # [Tk, D]
+        vg = v.data[keep][:, g, :].astype(np.float64)
+        qg = q.data[:, hs, :].astype(np.float64).reshape(tq * hs.size, d)
+        s = (qg @ kg.T).reshape(tq, hs.size, -1) * scale          # [Tq, G, Tk]
+        s = np.where(adm[:, None, :], s, NEG_INF)
+        mx = s.max(axis=2)
+        has = np.isfinite(mx)
+        base = np.where(has, mx, 0.0)
+        w = np.where(adm[:, None, :], np.exp(s - base[:, :, None]), 0.0)
+        den = w.sum(axis=2)
+        num = (w.reshape(tq * hs.size, -1) @ vg).reshape(tq, hs.size, d)
+        num /= np.where(has, den, 1.0)[:, :, None]
+        out[:, hs, :] = np.where(has[:, :, None], num, 0.0)
+        lse[:, hs] = np.where(has, base + np.log(np.where(has, den, 1.0)), NEG_INF)
+    return out, lse
+
+
+def sampled_rows_attention(q_rows: Blk, k: Blk, v: Blk, n_kv_heads: int, scale: float | None = None,
+                           block: int = 16384):
+    """Exact fp64 attention of a few query rows against a long key sequence:
+    the reference's recipe for large T — gqa_attention on
+    consecutive key blocks (attention.py:230-282), folded left in ascending
+    block order with merge_attention (attention.py:319-334).  Blocks whose
+    smallest valid position exceeds every query position admit nothing and
+    are skipped (merging an all -inf partial is the exact identity of
+    _merge_pair, attention.py:299-316).  Returns (out [R, Hq, D], lse [R, Hq])."""
+    parts = []
+    qmax = int(q_rows.pos[q_rows.valid].max()) if q_rows.valid.any() else -1
+    for a in range(0, k.n, block):
+        b = min(k.n, a + block)
+        kv = k.valid[a:b]
+        if not kv.any() or int(k.pos[a:b][kv].min()) > qmax:
+            continue
+        kb = Blk(k.data[a:b], k.pos[a:b], k.valid[a:b], k.seq[a:b])
+        vb = Blk(v.data[a:b], v.pos[a:b], v.valid[a:b], v.seq[a:b])
+        parts.append(gqa_grouped(q_rows, kb, vb, n_kv_heads, scale))
+    if not parts:
+        tq, hq, d = q_rows.data.shape
+        return np.zeros((tq, hq, d)), np.full((tq, hq), NEG_INF)
+    return merge(parts)
+
+
+def sample_rows(n_tokens: int, n_ranks: int, count: int, seed: int = 0) -> np.ndarray:
+    """Query rows worth checking at scale: first / last token, both sides of
+    every 2N-chunk boundary (sharding.py:144-151), then random rows up to
+    ``count`` (the boundaries are always included)."""
+    c = -(-n_tokens // (2 * n_ranks))
+    rows = {0, n_tokens - 1}
+    for m in range(1, 2 * n_ranks):
+        b = m * c
+        if 0 < b < n_tokens:
+            rows.update((b - 1, b))
+    rng = np.random.default_rng(seed)
+    while len(rows) < count and len(rows) < n_tokens:
+        rows.add(int(rng.integers(0, n_tokens)))
+    return np.array(sorted(rows), np.int64)

@@ -17,6 +17,9 @@ Cases:
   shard_*    plan_full_prefill / plan_partial_prefill / materialize_rank_block.
   decode_*   plan_decode assignments.
   ring_*     ring pass-KV composed from reference primitives (SPEC Alg. 2).
+  sampled_*  the large-T recipe: a few query rows against 16K-24K keys, blocked
+             gqa_attention + merge_attention and one unblocked call (inputs
+             regenerated from the stored seed).
 """
 
 from __future__ import annotations
@@ -49,13 +52,7 @@ from ringcp.sharding import (  # noqa: E402
 OUT = os.path.dirname(os.path.abspath(__file__))
 
 
-def bf16_exact(x: np.ndarray) -> np.ndarray:
-    """Round float32 to bf16 (round-to-nearest-even) and back to float32."""
-    x = np.asarray(x, np.float32)
-    u = x.view(np.uint32).astype(np.uint64)
-    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
-    return r.astype(np.uint32).view(np.float32)
-
+from make_golden_inputs import bf16_exact, sampled_inputs  # noqa: E402
 
 def blk(data, pos, valid=None, seq=None):
     n = len(pos)
@@ -280,6 +277,36 @@ def ring_cases():
     return store, names
 
 
+def sampled_cases():
+    """Large-T recipe: a few query rows against a long key
+    sequence, as gqa_attention over consecutive key blocks folded with
+    merge_attention (ascending), and as ONE gqa_attention call over all keys."""
+    store = {}
+    names = []
+    for name, seed, T, hq, hkv, block, rows in [
+        ("s24k_8x2", 5, 24576, 8, 2, 4096, [0, 1, 4095, 4096, 12287, 12288, 20000, 24575]),
+        ("s16k_16x1", 6, 16384, 16, 1, 5000, [0, 127, 128, 8191, 8192, 16383]),
+    ]:
+        rows = np.array(rows, np.int64)
+        q, k, v = sampled_inputs(seed, T, hq, hkv, rows)
+        cfg = GqaConfig(hq, hkv, 128)
+        qb = blk(q, rows)
+        parts = []
+        for a in range(0, T, block):
+            b = min(T, a + block)
+            parts.append(gqa_attention(qb, blk(k[a:b], np.arange(a, b)), blk(v[a:b], np.arange(a, b)), cfg))
+        merged = merge_attention(parts)
+        single = gqa_attention(qb, blk(k, np.arange(T)), blk(v, np.arange(T)), cfg)
+        store[f"{name}__meta"] = np.array([seed, T, hq, hkv, block])
+        store[f"{name}__rows"] = rows
+        store[f"{name}__out_blocked"] = np.asarray(merged.output.data)
+        store[f"{name}__lse_blocked"] = np.asarray(merged.lse)
+        store[f"{name}__out_single"] = np.asarray(single.output.data)
+        store[f"{name}__lse_single"] = np.asarray(single.lse)
+        names.append(name)
+    return store, names
+
+
 def main():
     g, gn = gqa_cases()
     np.savez_compressed(os.path.join(OUT, "gqa.npz"), names=np.array(gn), **g)
@@ -293,6 +320,8 @@ def main():
         json.dump(decode_cases(), f, indent=1)
     r, rn = ring_cases()
     np.savez_compressed(os.path.join(OUT, "ring.npz"), names=np.array(rn), **r)
+    sm, smn = sampled_cases()
+    np.savez_compressed(os.path.join(OUT, "sampled.npz"), names=np.array(smn), **sm)
     print("wrote golden fixtures:", sorted(os.listdir(OUT)))
 
 
