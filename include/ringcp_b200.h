@@ -90,6 +90,15 @@ int rcp_shard_gather(void* dst, const void* const* src_rows, const int64_t* new_
                      int32_t n_ranks, int32_t rank, int64_t row_bytes, int32_t* pos_out,
                      int32_t* seq_out, int32_t is_key, void* stream);
 
+/* Inverse of rcp_shard_gather (the device scatter of the load-balanced
+ * sharding, sharding.py:105-115, 211-240 read backwards): every VALID slot of
+ * rank `rank`'s block `src` (slot order, row_bytes per slot) is written to row
+ * `local` of sequence i's token-ordered array dst_rows[i] (HOST array of n_seqs
+ * device pointers); padding slots are dropped.  Run for every rank, the
+ * scatters tile each sequence exactly once. */
+int rcp_shard_scatter(void* const* dst_rows, const void* src, const int64_t* new_len, int32_t n_seqs,
+                      int32_t n_ranks, int32_t rank, int64_t row_bytes, void* stream);
+
 /* Row gather dst[i] = src[idx[i]] (idx < 0 -> zero row), idx int64 on device. */
 int rcp_gather_rows(void* dst, const void* src, const int64_t* idx, int64_t n_rows,
                     int64_t row_bytes, void* stream);

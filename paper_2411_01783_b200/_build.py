@@ -14,7 +14,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "_ringcp_b200.so")
-SOURCES = ["capi.cu", "attn_fwd.cu", "attn_variants.cu", "decode.cu"]
+SOURCES = ["capi.cu", "attn_fwd.cu", "attn_fwd_n128.cu", "attn_fwd_pair.cu", "decode.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -37,6 +37,7 @@ __all__ = [
 ]
 
 _INT32_MIN = -(2 ** 31)
+KERNEL_HEAD_DIM = 128  # head_dim of the attention / decode kernels; smaller heads are zero-padded
 
 
 def _device() -> torch.device:
@@ -324,19 +325,32 @@ def attend_into(q_data: torch.Tensor, q_meta, k_data: torch.Tensor, v_data: torc
 def gqa_attention(q: EmbeddingBlock, k: EmbeddingBlock, v: EmbeddingBlock, cfg: GqaConfig) -> PartialAttention:
     """Causal GQA attention of a query block against one key/value block
     (attention.py:230-282) on the tcgen05 kernel.  Key j is admitted for query i
-    iff both are valid, same sequence, and positions[j] <= positions[i]."""
+    iff both are valid, same sequence, and positions[j] <= positions[i].
+    head_dim <= 128 (smaller heads are zero-padded to the kernel's 128)."""
     if q.n_heads != cfg.n_query_heads or q.head_dim != cfg.head_dim:
         raise ValueError(f"query block is [{q.n_heads} x {q.head_dim}] but config wants "
                          f"[{cfg.n_query_heads} x {cfg.head_dim}]")
     _check_kv_pair(k, v, cfg)
+    if cfg.head_dim > KERNEL_HEAD_DIM:
+        raise ValueError(f"head_dim={cfg.head_dim} unsupported: the sm_100a kernels take head_dim <= "
+                         f"{KERNEL_HEAD_DIM}")
     if k.n_valid < k.n_tokens:  # drop padding before any arithmetic (attention.py:253-255)
         k, v = k.valid_only(), v.valid_only()
     tq = q.n_tokens
     dev = q.data.device
-    out = torch.empty((tq, cfg.n_query_heads, cfg.head_dim), dtype=torch.float32, device=dev)
+    qd, kd, vd = _bf16(q.data), _bf16(k.data), _bf16(v.data)
+    if cfg.head_dim < KERNEL_HEAD_DIM:
+        # Smaller heads (e.g. the reference tests' D = 4 / 8) run on the same
+        # kernel: zero columns change no Q.K dot product, the extra output
+        # columns are V's zeros and are sliced off; the scale stays cfg.scale.
+        pad = KERNEL_HEAD_DIM - cfg.head_dim
+        qd, kd, vd = (torch.nn.functional.pad(x, (0, pad)).contiguous() for x in (qd, kd, vd))
+    out = torch.empty((tq, cfg.n_query_heads, KERNEL_HEAD_DIM), dtype=torch.float32, device=dev)
     lse = torch.empty((tq, cfg.n_query_heads), dtype=torch.float32, device=dev)
-    attend_into(_bf16(q.data), q.meta32("q"), _bf16(k.data), _bf16(v.data), k.meta32("k"),
+    attend_into(qd, q.meta32("q"), kd, vd, k.meta32("k"),
                 cfg.n_query_heads, cfg.n_kv_heads, cfg.scale, out, lse, _lib.MODE_OVERWRITE)
+    if cfg.head_dim < KERNEL_HEAD_DIM:
+        out = out[:, :, :cfg.head_dim].contiguous()
     blk = EmbeddingBlock(out, q.positions, q.valid, q.seq_ids, validate=False, n_valid=q.n_valid)
     return PartialAttention(output=blk, lse=lse)
 

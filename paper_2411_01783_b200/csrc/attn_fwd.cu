@@ -548,18 +548,13 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
                 "workspace too small: need %zu bytes", need);
   RCP_CHECK_ARG((reinterpret_cast<uintptr_t>(workspace) & 31) == 0, "workspace must be 32-byte aligned");
 
-  // v4 (1-CTA, 64-key blocks) is the default: it measured best on the power-
-  // capped B200s ("Attention kernel versions").  RCP_ATTN_VERSION=5
-  // (CTA pairs), =6 (1-CTA, 128-key blocks, split softmax), =7 (Q in TMEM,
-  // TS-form S), =8 (CTA pairs, alternate-block softmax groups), =9
-  // (persistent v4), =10 (S decoupled from P in TMEM) and =11 (v10 + one MMA
-  // issuer per tile) are kept for A/B measurements; all pass the same parity
-  // tests.
+  // Kernel form: v12 (128-key blocks, attn_fwd_n128.cu) or v4 (64-key
+  // blocks, this file); RCP_ATTN_VERSION selects one for A/B measurements.
   static int version = -1;
   if (version < 0) {
     const char* e = getenv("RCP_ATTN_VERSION");
-    const int v = e ? atoi(e) : 4;
-    version = (v >= 5 && v <= 11) ? v : 4;
+    const int v = e ? atoi(e) : kDefaultAttnVersion;
+    version = (v == 4 || v == 12 || v == 13) ? v : kDefaultAttnVersion;
   }
   const int krows = attn_key_rows(version);
   AttnParams prm;
@@ -613,8 +608,10 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
 
   const int64_t grid = static_cast<int64_t>(prm.n_qblk) * hq;
   RCP_CHECK_ARG(grid < (1ll << 30), "grid too large");
-  if (version != 4) {
-    if ((rc = attn_variant_launch(version, prm, grid, st)) != RCP_OK) return rc;
+  if (version == 13) {
+    if ((rc = attn_pair_launch(prm, grid, st)) != RCP_OK) return rc;
+  } else if (version == 12) {
+    if ((rc = attn_n128_launch(prm, grid, st)) != RCP_OK) return rc;
   } else {
     static bool attr_set = false;
     if (!attr_set) {

@@ -1,6 +1,7 @@
 // C-ABI plumbing and the HBM-bound helper kernels of ringcp-b200:
 // error state, tile summaries, metadata folding, the N-way LSE merge (K2),
-// the empty-result fill and the row gathers behind materialize_rank_block (K0).
+// the empty-result fill, the row gathers behind materialize_rank_block (K0)
+// and its inverse scatter (rank slots -> token order).
 #include <climits>
 #include <cstring>
 #include <string>
@@ -142,6 +143,57 @@ __global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ Merg
   if (lane == 0) lse_out[row] = la_final;
 }
 
+// Fixed-N form of the merge (N = 2..8, the ring sizes): one warp per 32 rows.
+// Lane i first computes row i's whole chain of pairwise merge weights (the
+// same merge_weights calls, in the same order, as merge_kernel and the fused
+// attention epilogue, so the result is bitwise identical), keeping the
+// (wa, wb) of every step in registers; then the warp streams the 32 rows with
+// one float4 per lane, all N partial loads of a row issued before the fold
+// and the step weights broadcast by shuffles.  The weight chain (4 expf + 1
+// logf per step) is computed once per row instead of once per lane.
+template <int N>
+__global__ void __launch_bounds__(256) merge_rows32_kernel(const __grid_constant__ MergeArgs a, int64_t rows,
+                                                           float* __restrict__ o_out,
+                                                           float* __restrict__ lse_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row0 = ((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5) * 32;
+  if (row0 >= rows) return;
+  float wa[N], wb[N];
+  {
+    const int64_t r = row0 + lane;
+    float la = r < rows ? __ldg(a.lse[0] + r) : -INFINITY;
+    wa[0] = wb[0] = 0.f;
+#pragma unroll
+    for (int s = 1; s < N; ++s) {
+      const float lb = r < rows ? __ldg(a.lse[s] + r) : -INFINITY;
+      const MergeW w = merge_weights(la, lb);
+      wa[s] = w.wa;
+      wb[s] = w.wb;
+      la = w.lse;
+    }
+    if (r < rows) lse_out[r] = la;
+  }
+  const int64_t nr = rows - row0 < 32 ? rows - row0 : 32;
+  for (int rr = 0; rr < nr; ++rr) {
+    const int64_t row = row0 + rr;
+    float4 v[N];
+#pragma unroll
+    for (int s = 0; s < N; ++s) v[s] = __ldg(reinterpret_cast<const float4*>(a.o[s] + row * 128) + lane);
+    float4 acc = v[0];
+#pragma unroll
+    for (int s = 1; s < N; ++s) {
+      MergeW w;
+      w.wa = __shfl_sync(0xffffffffu, wa[s], rr);
+      w.wb = __shfl_sync(0xffffffffu, wb[s], rr);
+      acc.x = merge_val(acc.x, v[s].x, w);
+      acc.y = merge_val(acc.y, v[s].y, w);
+      acc.z = merge_val(acc.z, v[s].z, w);
+      acc.w = merge_val(acc.w, v[s].w, w);
+    }
+    reinterpret_cast<float4*>(o_out + row * 128)[lane] = acc;
+  }
+}
+
 // ------------------------------------------------------------------ gathers
 // Generic row gather, one warp per row, 16-byte vectors:
 // dst[i] = idx[i] >= 0 ? src[idx[i]] : 0.
@@ -209,6 +261,32 @@ __global__ void shard_gather_kernel(const __grid_constant__ ShardArgs a, int32_t
   }
 }
 
+// Inverse of shard_gather_kernel (the scatter half of materialize_rank_block,
+// sharding.py:105-115, 211-240): every VALID slot of this rank's block goes
+// back to row `local` of its sequence's token-ordered array; padding slots are
+// dropped.  Each destination row is written by exactly one (rank, slot), so
+// the N ranks' scatters tile the sequence.
+// (ShardArgs.src carries the per-sequence DESTINATION rows here.)
+__global__ void shard_scatter_kernel(const __grid_constant__ ShardArgs a, int32_t n_seqs, int32_t n_ranks,
+                                     int32_t rank, int64_t vec_per_row, const uint4* __restrict__ src) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total_slots = a.slot_begin[n_seqs];
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t slot = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+       slot < total_slots; slot += warps) {
+    int sq = 0;
+    while (sq + 1 < n_seqs && a.slot_begin[sq + 1] <= slot) ++sq;
+    const int64_t s = slot - a.slot_begin[sq];
+    const int64_t ch = a.chunk[sq];
+    const int64_t chunk_id = s < ch ? rank : 2 * n_ranks - 1 - rank;
+    const int64_t local = chunk_id * ch + (s < ch ? s : s - ch);
+    if (local >= a.new_len[sq]) continue;  // warp-uniform
+    const uint4* sp = src + slot * vec_per_row;
+    uint4* d = const_cast<uint4*>(a.src[sq]) + local * vec_per_row;
+    for (int64_t c = lane; c < vec_per_row; c += 32) d[c] = __ldg(sp + c);
+  }
+}
+
 static unsigned grid_for(int64_t work, int threads) {
   int64_t b = (work + threads - 1) / threads;
   const int64_t cap = 148 * 16;
@@ -265,10 +343,24 @@ int rcp_merge_attn(const float* const* o_parts, const float* const* lse_parts, i
     a.o[i] = o_parts[i];
     a.lse[i] = lse_parts[i];
   }
-  const int64_t threads = rows * 32;
-  const unsigned blocks = static_cast<unsigned>((threads + 255) / 256);
-  merge_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, n, rows, head_dim / 4, o_out,
-                                                                   lse_out);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (head_dim == 128 && n >= 2 && n <= 8) {
+    const int64_t warps = (rows + 31) / 32;
+    const unsigned blocks = static_cast<unsigned>((warps + 7) / 8);
+    switch (n) {
+      case 2: merge_rows32_kernel<2><<<blocks, 256, 0, st>>>(a, rows, o_out, lse_out); break;
+      case 3: merge_rows32_kernel<3><<<blocks, 256, 0, st>>>(a, rows, o_out, lse_out); break;
+      case 4: merge_rows32_kernel<4><<<blocks, 256, 0, st>>>(a, rows, o_out, lse_out); break;
+      case 5: merge_rows32_kernel<5><<<blocks, 256, 0, st>>>(a, rows, o_out, lse_out); break;
+      case 6: merge_rows32_kernel<6><<<blocks, 256, 0, st>>>(a, rows, o_out, lse_out); break;
+      case 7: merge_rows32_kernel<7><<<blocks, 256, 0, st>>>(a, rows, o_out, lse_out); break;
+      default: merge_rows32_kernel<8><<<blocks, 256, 0, st>>>(a, rows, o_out, lse_out); break;
+    }
+  } else {
+    const int64_t threads = rows * 32;
+    const unsigned blocks = static_cast<unsigned>((threads + 255) / 256);
+    merge_kernel<<<blocks, 256, 0, st>>>(a, n, rows, head_dim / 4, o_out, lse_out);
+  }
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
 }
@@ -318,6 +410,35 @@ int rcp_shard_gather(void* dst, const void* const* src_rows, const int64_t* new_
   const int64_t vpr = row_bytes / 16;
   shard_gather_kernel<<<grid_for(slot * 32, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       a, n_seqs, n_ranks, rank, vpr, static_cast<uint4*>(dst), pos_out, seq_out, is_key);
+  RCP_CUDA(cudaGetLastError());
+  return RCP_OK;
+}
+
+int rcp_shard_scatter(void* const* dst_rows, const void* src, const int64_t* new_len, int32_t n_seqs,
+                      int32_t n_ranks, int32_t rank, int64_t row_bytes, void* stream) {
+  RCP_CHECK_ARG(n_ranks >= 1, "n_ranks must be >= 1");
+  RCP_CHECK_ARG(rank >= 0 && rank < n_ranks, "rank %d out of range for %d ranks", rank, n_ranks);
+  RCP_CHECK_ARG(n_seqs >= 1, "cannot plan an empty sequence list");
+  RCP_CHECK_ARG(n_seqs <= kMaxShardSeqs, "at most %d sequences per scatter", kMaxShardSeqs);
+  RCP_CHECK_ARG(row_bytes > 0 && row_bytes % 16 == 0, "row_bytes must be a positive multiple of 16");
+  RCP_CHECK_ARG((reinterpret_cast<uintptr_t>(src) & 15) == 0, "src must be 16-byte aligned");
+  ShardArgs a;
+  memset(&a, 0, sizeof(a));
+  int64_t slot = 0;
+  for (int i = 0; i < n_seqs; ++i) {
+    RCP_CHECK_ARG(new_len[i] >= 1, "sequence %d has no new tokens", i);
+    RCP_CHECK_ARG((reinterpret_cast<uintptr_t>(dst_rows[i]) & 15) == 0,
+                  "destination of sequence %d must be 16-byte aligned", i);
+    a.src[i] = static_cast<const uint4*>(dst_rows[i]);
+    a.chunk[i] = (new_len[i] + 2 * n_ranks - 1) / (2 * n_ranks);
+    a.new_len[i] = new_len[i];
+    a.slot_begin[i] = slot;
+    slot += 2 * a.chunk[i];
+  }
+  a.slot_begin[n_seqs] = slot;
+  const int64_t vpr = row_bytes / 16;
+  shard_scatter_kernel<<<grid_for(slot * 32, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      a, n_seqs, n_ranks, rank, vpr, static_cast<const uint4*>(src));
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
 }

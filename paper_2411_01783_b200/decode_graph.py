@@ -36,6 +36,12 @@ from .sharding import plan_decode
 
 __all__ = ["GraphedDecode"]
 
+
+def _lens_slice(g) -> slice:
+    """Slice of the lens section in the step metadata (rows | starts | lens | pos | seq)."""
+    S, R = g.slots, g.n * g.slots
+    return slice(S + R, S + 2 * R)
+
 _SCRATCH_SEQ = -7  # cache-internal sequence id of the scratch row (never a query's id)
 
 
@@ -89,6 +95,21 @@ class GraphedDecode:
                               dtype=torch.uint8, device=dev)
         self.graph = None
         self._arena_ptr = None
+        self._segs_at_capture = None
+
+    def _segment_key(self):
+        """(start, capacity) of every batch sequence's arena segment: the
+        captured decode launch's split bound (max_len) covers these only."""
+        return tuple((self.cache._segs[s].start, self.cache._segs[s].cap) for s in self.batch)
+
+    def _refit(self) -> None:
+        """Re-derive the split bound and workspace from the current segments
+        (a segment moved or grew between steps, e.g. an eager append)."""
+        self.max_len = max(self.cache._segs[s].cap for s in self.batch)
+        need = int(_lib.load().rcp_decode_workspace_bytes(self.n * self.slots, self.cfg.n_query_heads,
+                                                          self.max_len))
+        if self.ws.numel() < need:
+            self.ws = torch.empty(need, dtype=torch.uint8, device=self.cache.device)
 
     # ------------------------------------------------------------------ launches
     def _launches(self):
@@ -123,6 +144,7 @@ class GraphedDecode:
         self.graph = g
         self._arena_ptr = (self.cache.k.data_ptr(), self.cache.v.data_ptr(), self.cache.pos.data_ptr(),
                            self.cache.seq.data_ptr())
+        self._segs_at_capture = self._segment_key()
 
     # ------------------------------------------------------------------ per step
     def _host_meta(self, mine, positions):
@@ -163,6 +185,11 @@ class GraphedDecode:
         _lib.h2d(meta, self.cache.device, out=self.meta)  # ordered after the previous replay
         ptrs = (self.cache.k.data_ptr(), self.cache.v.data_ptr(), self.cache.pos.data_ptr(),
                 self.cache.seq.data_ptr())
+        if self.graph is not None and self._segment_key() != self._segs_at_capture:
+            self._refit()  # a segment moved / grew since capture: the baked split bound is stale
+            self.graph = None
+        if max(int(x) for x in meta[_lens_slice(self)]) > self.max_len:
+            raise RuntimeError("GraphedDecode: a KV segment exceeds the captured split bound")
         if self.graph is None or ptrs != self._arena_ptr:
             # the warm-up launch in _capture executes this step (capture only
             # records), so the step's appends and outputs happen exactly once

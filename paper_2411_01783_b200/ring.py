@@ -345,7 +345,10 @@ class TorchRingComm:
     waits for work already queued, so a transfer issued before a step's kernel
     overlaps it; ``wait`` makes the current stream wait for the transfer."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, timeout_s: float | None = None):
+        import datetime
+        import os
+
         import torch.distributed as dist
 
         self.dist = dist
@@ -353,6 +356,15 @@ class TorchRingComm:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.topo = RingTopology(self.world)
+        # Deadline of one ring transfer.  Host-blocking backends (gloo) raise
+        # when it passes; for NCCL ``wait`` only orders the stream, and the
+        # process group's watchdog (init_process_group(timeout=...)) enforces
+        # the deadline on the device side, while ``wait_done`` below gives a
+        # host-side deadline that aborts the communicator.
+        t = timeout_s if timeout_s is not None else float(os.environ.get("RCP_COMM_TIMEOUT_S", "600"))
+        self.timeout_s = t
+        self._timeout = datetime.timedelta(seconds=t)
+        self._stream_ordered = dist.get_backend(group) == "nccl"
 
     def _g(self, r: int) -> int:
         return r if self.group is None else self.dist.get_global_rank(self.group, r)
@@ -413,10 +425,48 @@ class TorchRingComm:
             recvs[self.rank].copy_(sends[self.rank])
         return works
 
-    @staticmethod
-    def wait(works):
+    def wait(self, works):
+        if self._stream_ordered:
+            # NCCL: make the current stream wait, never the host (a timed wait
+            # would block the host until the transfer lands and serialise the
+            # ring); deadlines are the watchdog's / wait_done's job
+            for w in works or []:
+                w.wait()
+            return
         for w in works or []:
-            w.wait()
+            try:
+                ok = w.wait(self._timeout)
+            except RuntimeError as e:
+                ok = False
+                err = e
+            else:
+                err = None
+            if not ok:
+                self.abort()
+                raise RuntimeError(f"ring transfer not complete after {self.timeout_s} s (peer hung?); "
+                                   "communicator aborted") from err
+
+    def abort(self) -> None:
+        """Abort the communicator (a hung peer must not block this rank forever)."""
+        from torch.distributed.distributed_c10d import _abort_process_group
+
+        try:
+            _abort_process_group(self.group)
+        except Exception:  # noqa: BLE001 - best effort; the caller raises anyway
+            pass
+
+    def wait_done(self, event, timeout_s: float | None = None, poll_s: float = 1e-3) -> None:
+        """Host-side deadline for stream work (e.g. an event recorded after a
+        ring step): poll until it completes; past the deadline abort the
+        communicator and raise instead of blocking forever."""
+        import time
+
+        limit = time.monotonic() + (self.timeout_s if timeout_s is None else timeout_s)
+        while not event.query():
+            if time.monotonic() > limit:
+                self.abort()
+                raise RuntimeError("ring step did not complete before the deadline; communicator aborted")
+            time.sleep(poll_s)
 
 
 # ------------------------------------------------------------------ compute hooks
@@ -546,6 +596,7 @@ class RingAttention:
                     t.record_stream(self._side_stream(name))
             t = torch.empty(shape, dtype=dtype, device=device)
             self._bufs[key] = t
+            self._bufs[("realloc",)] = True
         return t
 
     def _next_slot(self, kind: str) -> int:
@@ -602,9 +653,15 @@ class RingAttention:
         qp = self._slot_tensor(("stage", slot, "qp"), (S,), torch.int32, device)
         qs = self._slot_tensor(("stage", slot, "qs"), (S,), torch.int32, device)
         free = self._bufs.get(("stage", slot, "free"))
+        realloc = self._bufs.pop(("realloc",), False)
         with torch.cuda.stream(s_in):
             if free is not None:  # the compute that last read this slot is done
                 s_in.wait_event(free)
+            if realloc:
+                # a staging tensor was (re)allocated on the compute stream: its
+                # memory may be a block the compute stream freed while still in
+                # use by queued kernels, so the copies must follow that work
+                s_in.wait_stream(torch.cuda.current_stream(device))
 
             def fill(dst, srcs, a, b):
                 flat = dst.view(dst.shape[0], -1)
@@ -617,10 +674,12 @@ class RingAttention:
 
             fill(kd, k_host, 0, S)
             fill(vd, v_host, 0, S)
-            kv_ready = torch.cuda.Event(enable_timing=True)  # timing: tools/e2e_loop_ranges.py
-            kv_ready.record(s_in)
+            # the slot positions go with the K/V: the cache append reads them
+            # (append_new_tokens(slot_pos=qp)) after waiting only on kv_ready
             _lib.h2d(posv.astype(np.int32), device, out=qp)
             _lib.h2d(seqv.astype(np.int32), device, out=qs)
+            kv_ready = torch.cuda.Event(enable_timing=True)  # timing: tools/e2e_loop_ranges.py
+            kv_ready.record(s_in)
             q_ready = []
             for a, b in splits:
                 fill(q, q_host, a, b)

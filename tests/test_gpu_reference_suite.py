@@ -1,0 +1,324 @@
+"""The reference's own attention test suite (pkg/tests/test_attention.py:32-280)
+run through the device drop-in API on the sm_100a kernels.
+
+Same geometries (head_dim 4 / 8, zero-padded to the kernel's 128 at the API
+boundary), same seeds, same structure.  Where the reference is bitwise, so is
+this port (padding invisibility, merge([p]) is p, one-pass == nested merge,
+all-masked partials, the single-key row); where it compares fp64 numerics
+with 1e-6 / 1e-9 tolerances, this port compares the bf16-input kernel with the
+north-star tolerance (|dO| <= 2e-2, |dLSE| <= 1e-3) on bf16-exact inputs
+against the fp64 oracle (the reference algorithm restated, pinned to the
+reference's golden vectors in tests/test_oracle_golden.py).
+"""
+
+import math
+
+import numpy as np
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+from oracle import ringcp_oracle as orc
+from tests import _golden as G
+from tests.golden.make_golden_inputs import bf16_exact
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rc():
+    import paper_2411_01783_b200 as rc
+
+    return rc
+
+
+def make_block(rc, rng, n_tokens, n_heads, head_dim, positions=None, seq_id=0):
+    """test_attention.py:19-23, with the data rounded to bf16 (what the kernels consume)."""
+    data = bf16_exact(rng.standard_normal((n_tokens, n_heads, head_dim)).astype(np.float32))
+    if positions is None:
+        positions = np.arange(n_tokens)
+    return rc.EmbeddingBlock.from_tokens(data, positions, seq_id=seq_id)
+
+
+def host(b):
+    d, p, v, s = b.to_numpy()
+    return orc.Blk(d, p, v, s)
+
+
+def np_out(part):
+    return part.output.data.double().cpu().numpy(), part.lse.double().cpu().numpy()
+
+
+def slice_block(rc, block, lo, hi):
+    return rc.EmbeddingBlock(block.data[lo:hi], block.positions[lo:hi], block.valid[lo:hi], block.seq_ids[lo:hi])
+
+
+# ------------------------------------------------------------------ TestGqaAttention
+def test_single_admitted_key_returns_value_row_exactly(rc):
+    """test_attention.py:32-46: one admitted key -> weight exactly 1 -> O is V's row bitwise."""
+    cfg = rc.GqaConfig(n_query_heads=2, n_kv_heads=1, head_dim=4)
+    rng = np.random.default_rng(0)
+    q = make_block(rc, rng, 1, 2, 4, positions=[5])
+    k = make_block(rc, rng, 1, 1, 4, positions=[3])
+    v = make_block(rc, rng, 1, 1, 4, positions=[3])
+    out, lse = np_out(rc.gqa_attention(q, k, v, cfg))
+    vrow = v.data.cpu().numpy()[0, 0].astype(np.float64)
+    qd, kd = q.data.cpu().numpy().astype(np.float64), k.data.cpu().numpy().astype(np.float64)
+    for h in range(2):
+        np.testing.assert_array_equal(out[0, h], vrow)
+        assert lse[0, h] == pytest.approx(cfg.scale * float(np.dot(qd[0, h], kd[0, 0])), abs=1e-5)
+
+
+def test_fully_masked_row_is_zero_with_neg_inf_lse(rc):
+    """test_attention.py:48-56."""
+    cfg = rc.GqaConfig(n_query_heads=1, n_kv_heads=1, head_dim=4)
+    rng = np.random.default_rng(1)
+    q = make_block(rc, rng, 1, 1, 4, positions=[3])
+    k = make_block(rc, rng, 1, 1, 4, positions=[5])
+    v = make_block(rc, rng, 1, 1, 4, positions=[5])
+    out, lse = np_out(rc.gqa_attention(q, k, v, cfg))
+    assert np.all(out == 0.0)
+    assert np.all(np.isneginf(lse))
+
+
+def test_matches_nested_loop_oracle_on_causal_self_attention(rc):
+    """test_attention.py:58-70 (nested-loop oracle = pkg/tests/reference.py)."""
+    cfg = rc.GqaConfig(n_query_heads=4, n_kv_heads=2, head_dim=8)
+    rng = np.random.default_rng(7)
+    q = make_block(rc, rng, 8, 4, 8)
+    k = make_block(rc, rng, 8, 2, 8)
+    v = make_block(rc, rng, 8, 2, 8)
+    out, lse = np_out(rc.gqa_attention(q, k, v, cfg))
+    hq, hk, hv = host(q), host(k), host(v)
+    want_out, want_lse = orc.naive_gqa_loops(hq.data, hk.data, hv.data, hq.pos, hk.pos, 2, cfg.scale)
+    assert np.abs(out - want_out).max() <= G.O_TOL
+    assert G.lse_err(lse, want_lse) <= G.LSE_TOL
+
+
+def test_cross_sequence_keys_are_never_admitted(rc):
+    """test_attention.py:72-79."""
+    cfg = rc.GqaConfig(n_query_heads=2, n_kv_heads=2, head_dim=4)
+    rng = np.random.default_rng(3)
+    q = make_block(rc, rng, 3, 2, 4, seq_id=1)
+    k_other = make_block(rc, rng, 4, 2, 4, seq_id=2)
+    _, lse = np_out(rc.gqa_attention(q, k_other, k_other, cfg))
+    assert np.all(np.isneginf(lse))
+    assert rc.admitted_pair_count(q, k_other) == 0
+
+
+def test_padding_rows_change_nothing_bitwise(rc):
+    """test_attention.py:81-106: padding inserted anywhere in K/V changes no output bit."""
+    import torch
+
+    cfg = rc.GqaConfig(n_query_heads=4, n_kv_heads=2, head_dim=8)
+    rng = np.random.default_rng(11)
+    q = make_block(rc, rng, 6, 4, 8)
+    k = make_block(rc, rng, 6, 2, 8)
+    v = make_block(rc, rng, 6, 2, 8)
+    base = np_out(rc.gqa_attention(q, k, v, cfg))
+
+    def with_padding(block, where):
+        pad = rc.EmbeddingBlock.padding(2, block.n_heads, block.head_dim)
+        cat = lambda a, b: torch.cat([a[:where], b, a[where:]])
+        return rc.EmbeddingBlock(cat(block.data, pad.data), cat(block.positions, pad.positions),
+                                 cat(block.valid, pad.valid), cat(block.seq_ids, pad.seq_ids))
+
+    for where in (0, 3, 6):
+        out, lse = np_out(rc.gqa_attention(q, with_padding(k, where), with_padding(v, where), cfg))
+        np.testing.assert_array_equal(out, base[0])
+        np.testing.assert_array_equal(lse, base[1])
+
+
+def test_softmax_weights_recovered_from_lse_sum_to_one(rc):
+    """test_attention.py:108-125: sum_j exp(s_ij - lse_i) == 1 (fp32 LSE: to 1e-4)."""
+    cfg = rc.GqaConfig(n_query_heads=4, n_kv_heads=4, head_dim=8)
+    rng = np.random.default_rng(23)
+    q = make_block(rc, rng, 10, 4, 8)
+    k = make_block(rc, rng, 10, 4, 8)
+    v = make_block(rc, rng, 10, 4, 8)
+    _, lse = np_out(rc.gqa_attention(q, k, v, cfg))
+    q64, k64 = host(q).data.astype(np.float64), host(k).data.astype(np.float64)
+    for i in range(10):
+        for h in range(4):
+            scores = [cfg.scale * np.dot(q64[i, h], k64[j, h]) for j in range(10) if j <= i]
+            total = sum(math.exp(s - lse[i, h]) for s in scores)
+            assert total == pytest.approx(1.0, abs=1e-4)
+
+
+def test_shape_and_divisibility_errors(rc):
+    """test_attention.py:127-139 (same ValueError substrings)."""
+    with pytest.raises(ValueError, match="divisible"):
+        rc.GqaConfig(n_query_heads=3, n_kv_heads=2, head_dim=4)
+    cfg = rc.GqaConfig(n_query_heads=2, n_kv_heads=1, head_dim=4)
+    rng = np.random.default_rng(5)
+    q = make_block(rc, rng, 2, 2, 4)
+    k = make_block(rc, rng, 2, 1, 4)
+    v_bad = make_block(rc, rng, 3, 1, 4)
+    with pytest.raises(ValueError, match="mismatch"):
+        rc.gqa_attention(q, k, v_bad, cfg)
+    k_bad_heads = make_block(rc, rng, 2, 2, 4)
+    with pytest.raises(ValueError):
+        rc.gqa_attention(q, k_bad_heads, k_bad_heads, cfg)
+
+
+def test_head_dim_above_kernel_limit_is_rejected(rc):
+    """Drop-in limit: head_dim <= 128; larger heads raise before any compute."""
+    cfg = rc.GqaConfig(n_query_heads=2, n_kv_heads=1, head_dim=256)
+    rng = np.random.default_rng(5)
+    q = make_block(rc, rng, 2, 2, 256)
+    k = make_block(rc, rng, 2, 1, 256)
+    with pytest.raises(ValueError, match="head_dim"):
+        rc.gqa_attention(q, k, k, cfg)
+
+
+# ------------------------------------------------------------------ TestMergeAttention
+def _parts_from_split(rc, rng, n_keys, split_at, cfg):
+    q = make_block(rc, rng, 4, cfg.n_query_heads, cfg.head_dim, positions=np.arange(n_keys, n_keys + 4))
+    k = make_block(rc, rng, n_keys, cfg.n_kv_heads, cfg.head_dim)
+    v = make_block(rc, rng, n_keys, cfg.n_kv_heads, cfg.head_dim)
+    whole = rc.gqa_attention(q, k, v, cfg)
+    parts = [rc.gqa_attention(q, slice_block(rc, k, lo, hi), slice_block(rc, v, lo, hi), cfg)
+             for lo, hi in [(0, split_at), (split_at, n_keys)]]
+    return whole, parts
+
+
+def test_single_part_is_identity(rc):
+    """test_attention.py:163-169."""
+    cfg = rc.GqaConfig(n_query_heads=2, n_kv_heads=2, head_dim=4)
+    rng = np.random.default_rng(2)
+    q = make_block(rc, rng, 3, 2, 4)
+    part = rc.gqa_attention(q, q, q, cfg)
+    assert rc.merge_attention([part]) is part
+
+
+def test_two_parts_with_equal_lse_average_outputs(rc):
+    """test_attention.py:171-187 (fp32 merge: to 1e-6 relative)."""
+    rng = np.random.default_rng(4)
+    lse_val = 0.75
+    mk = lambda: rc.PartialAttention(
+        output=rc.EmbeddingBlock.from_tokens(rng.standard_normal((3, 2, 4)).astype(np.float32), np.arange(3)),
+        lse=np.full((3, 2), lse_val, np.float32))
+    p1, p2 = mk(), mk()
+    merged = rc.merge_attention([p1, p2])
+    a, b = p1.output.data.double().cpu().numpy(), p2.output.data.double().cpu().numpy()
+    np.testing.assert_allclose(merged.output.data.double().cpu().numpy(), (a + b) / 2, rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(merged.lse.double().cpu().numpy(), np.float32(lse_val) + math.log(2), rtol=1e-6)
+
+
+def test_split_merge_matches_unsplit_attention(rc):
+    """test_attention.py:189-195."""
+    cfg = rc.GqaConfig(n_query_heads=4, n_kv_heads=2, head_dim=8)
+    rng = np.random.default_rng(6)
+    whole, parts = _parts_from_split(rc, rng, 16, 8, cfg)
+    mo, ml = np_out(rc.merge_attention(parts))
+    wo, wl = np_out(whole)
+    assert np.abs(mo - wo).max() <= G.O_TOL
+    assert G.lse_err(ml, wl) <= G.LSE_TOL
+
+
+def test_one_pass_merge_equals_nested_pairwise_bitwise(rc):
+    """test_attention.py:197-208: a left fold in one call == nested pairwise merges, bitwise."""
+    cfg = rc.GqaConfig(n_query_heads=4, n_kv_heads=2, head_dim=8)
+    rng = np.random.default_rng(8)
+    q = make_block(rc, rng, 5, 4, 8, positions=np.arange(12, 17))
+    parts = []
+    for lo in range(0, 12, 4):
+        k = make_block(rc, rng, 4, 2, 8, positions=np.arange(lo, lo + 4))
+        parts.append(rc.gqa_attention(q, k, k, cfg))
+    one = np_out(rc.merge_attention(parts))
+    nested = np_out(rc.merge_attention([rc.merge_attention(parts[:2]), parts[2]]))
+    np.testing.assert_array_equal(one[0], nested[0])
+    np.testing.assert_array_equal(one[1], nested[1])
+
+
+def test_merge_handles_all_masked_partials(rc):
+    """test_attention.py:210-223 (bitwise)."""
+    cfg = rc.GqaConfig(n_query_heads=2, n_kv_heads=1, head_dim=4)
+    rng = np.random.default_rng(9)
+    q = make_block(rc, rng, 2, 2, 4, positions=[0, 1])
+    k_future = make_block(rc, rng, 2, 1, 4, positions=[5, 6])
+    k_past = make_block(rc, rng, 2, 1, 4, positions=[0, 1])
+    blank = rc.gqa_attention(q, k_future, k_future, cfg)
+    real = rc.gqa_attention(q, k_past, k_past, cfg)
+    mo, ml = np_out(rc.merge_attention([blank, real]))
+    ro, rl = np_out(real)
+    np.testing.assert_array_equal(mo, ro)
+    np.testing.assert_array_equal(ml, rl)
+    bo, bl = np_out(rc.merge_attention([blank, blank]))
+    assert np.all(np.isneginf(bl))
+    assert np.all(bo == 0.0)
+
+
+def test_merge_errors(rc):
+    """test_attention.py:225-235."""
+    with pytest.raises(ValueError, match="empty"):
+        rc.merge_attention([])
+    cfg = rc.GqaConfig(n_query_heads=2, n_kv_heads=2, head_dim=4)
+    rng = np.random.default_rng(10)
+    a = rc.gqa_attention(make_block(rc, rng, 2, 2, 4), make_block(rc, rng, 2, 2, 4), make_block(rc, rng, 2, 2, 4), cfg)
+    b = rc.gqa_attention(make_block(rc, rng, 3, 2, 4), make_block(rc, rng, 3, 2, 4), make_block(rc, rng, 3, 2, 4), cfg)
+    with pytest.raises(ValueError):
+        rc.merge_attention([a, b])
+
+
+# ------------------------------------------------------------------ property test
+@settings(deadline=None, max_examples=40)
+@given(seed=st.integers(0, 2 ** 32 - 1), n_keys=st.integers(1, 24), n_blocks=st.integers(1, 5),
+       n_kv_heads=st.sampled_from([1, 2, 4]))
+def test_block_split_invariance(seed, n_keys, n_blocks, n_kv_heads):
+    """test_attention.py:238-280: any partition of the key set (empty blocks
+    included), attended per block then merged, matches single-shot attention."""
+    import paper_2411_01783_b200 as rc
+
+    cfg = rc.GqaConfig(n_query_heads=4, n_kv_heads=n_kv_heads, head_dim=8)
+    rng = np.random.default_rng(seed)
+    q = make_block(rc, rng, 6, 4, 8, positions=np.arange(n_keys, n_keys + 6))
+    k = make_block(rc, rng, n_keys, n_kv_heads, 8)
+    v = make_block(rc, rng, n_keys, n_kv_heads, 8)
+    cuts = sorted(rng.integers(0, n_keys + 1, size=n_blocks - 1).tolist())
+    bounds = [0] + cuts + [n_keys]
+    parts = []
+    for lo, hi in zip(bounds, bounds[1:]):
+        if lo == hi:
+            e = rc.EmbeddingBlock.padding(0, n_kv_heads, 8)
+            parts.append(rc.gqa_attention(q, e, e, cfg))
+        else:
+            parts.append(rc.gqa_attention(q, slice_block(rc, k, lo, hi), slice_block(rc, v, lo, hi), cfg))
+    mo, ml = np_out(rc.merge_attention(parts))
+    wo, wl = np_out(rc.gqa_attention(q, k, v, cfg))
+    assert np.abs(mo - wo).max() <= G.O_TOL
+    assert G.lse_err(ml, wl) <= G.LSE_TOL
+    # and both match the fp64 oracle
+    oo, ol = orc.gqa(host(q), host(k), host(v), n_kv_heads, cfg.scale)
+    assert np.abs(wo - oo).max() <= G.O_TOL
+    assert G.lse_err(wl, ol) <= G.LSE_TOL
+
+
+# ------------------------------------------------------------------ API surface not covered above
+def test_admitted_pair_count_matches_reference_golden(rc):
+    """admitted_pair_count (attention.py:209-211) on device vs the reference's own counts."""
+    z = G.npz("gqa.npz")
+    for name in z["names"]:
+        c = G.gqa_case(z, name)
+        q = rc.EmbeddingBlock(c["q"].data, c["q"].pos, c["q"].valid, c["q"].seq)
+        k = rc.EmbeddingBlock(c["k"].data, c["k"].pos, c["k"].valid, c["k"].seq)
+        assert rc.admitted_pair_count(q, k) == c["pairs"], name
+
+
+@pytest.mark.parametrize("data,pos,valid,seq,msg", [
+    ([[[np.nan]], [[0.0]]], [0, 1], [True, True], [0, 0], "non-finite"),
+    ([[[1.0]], [[0.0]]], [-3, 1], [True, True], [0, 0], "non-negative positions"),
+    ([[[1.0]], [[0.0]]], [4, 4], [True, True], [0, 0], "not strictly increasing within sequence 0"),
+    ([[[1.0]], [[0.0]], [[2.0]]], [4, 9, 2], [True, True, True], [7, 7, 7], "not strictly increasing within sequence 7"),
+])
+def test_embedding_block_validation_messages(rc, data, pos, valid, seq, msg):
+    """EmbeddingBlock.__post_init__ checks (attention.py:85-106), same messages."""
+    with pytest.raises(ValueError, match=msg):
+        rc.EmbeddingBlock(np.array(data, np.float32), np.array(pos), np.array(valid), np.array(seq))
+
+
+def test_embedding_block_validation_ignores_padding_rows(rc):
+    """Invalid rows may hold anything (NaN data, -1 positions, repeated positions)."""
+    b = rc.EmbeddingBlock(np.array([[[np.nan]], [[1.0]], [[2.0]]], np.float32), np.array([-1, 0, 1]),
+                          np.array([False, True, True]), np.array([-1, 0, 0]))
+    assert b.n_valid == 2

@@ -212,3 +212,71 @@ def test_decode_kernel_vs_oracle(rc, hq, hkv, lens):
         wo, wl = orc.gqa(qb, kb, vb, hkv)
         assert np.abs(out[b].cpu().numpy() - wo[0]).max() <= G.O_TOL
         assert G.lse_err(lse[b].cpu().numpy(), wl[0]) <= G.LSE_TOL
+
+
+@pytest.mark.parametrize("lens,n,cached", [([4096], 2, [0]), ([1000, 333], 4, [0, 0]), ([8192], 8, [0]),
+                                           ([9], 4, [0]), ([700, 50, 2000], 3, [100, 0, 7])])
+def test_shard_scatter_inverts_gather_bit_exact(rc, lens, n, cached):
+    """Device scatter (rcp_shard_scatter) is the exact inverse of the device
+    gather: the N ranks' scatters rebuild every sequence bitwise, and each
+    rank's scatter writes exactly the oracle's local indices of that rank."""
+    import torch
+
+    from paper_2411_01783_b200.sharding import (SequenceSpec, materialize_rank_block, plan_partial_prefill,
+                                                scatter_rank_block, unshard)
+
+    rng = np.random.default_rng(sum(lens) + n)
+    specs = [SequenceSpec(i + 3, c, t) for i, (t, c) in enumerate(zip(lens, cached))]
+    layout = [[c // n + (1 if r < c % n else 0) for r in range(n)] for c in cached]
+    plan = plan_partial_prefill(specs, n, layout)
+    for shape, dt in (((2, 128), np.float32), ((8, 128), np.float32), ((1, 4), np.float32), ((1, 2), np.float32)):
+        xs = [rng.standard_normal((t,) + shape).astype(dt) for t in lens]
+        xd = [torch.from_numpy(x).cuda() for x in xs]
+        blocks = [materialize_rank_block(plan, r, xd).data for r in range(n)]
+        back = unshard(plan, blocks)
+        for x, b in zip(xs, back):
+            np.testing.assert_array_equal(b.cpu().numpy(), x)
+        # one rank alone writes exactly its own rows (others untouched)
+        for r in range(n):
+            outs = [torch.full((t,) + shape, -7.0, device="cuda") for t in lens]
+            scatter_rank_block(plan, r, blocks[r], outs)
+            for i, (x, o) in enumerate(zip(xs, outs)):
+                loc = orc.local_indices(lens[i], n, r)
+                loc = loc[loc >= 0]
+                got = o.cpu().numpy()
+                np.testing.assert_array_equal(got[loc], x[loc])
+                mask = np.ones(lens[i], bool)
+                mask[loc] = False
+                assert np.all(got[mask] == -7.0)
+
+
+def test_ring_outputs_unshard_to_token_order(rc):
+    """End to end: a simulated CP3 ring's slot-ordered outputs (O fp32 rows and
+    LSE rows), scattered back to token order on the device, match the oracle's
+    token-ordered single-block attention."""
+    import torch
+
+    from paper_2411_01783_b200.kv_cache import RankKvCache
+    from paper_2411_01783_b200.ring import ring_pass_kv_prefill
+    from paper_2411_01783_b200.sharding import SequenceSpec, materialize_rank_block, plan_full_prefill, unshard
+
+    T, n, hq, hkv = 1000, 3, 8, 2
+    rng = np.random.default_rng(5)
+    arrs = [_bf16_exact(rng.standard_normal((T, h, 128)).astype(np.float32)) for h in (hq, hkv, hkv)]
+    dev = [torch.from_numpy(a).cuda().to(torch.bfloat16) for a in arrs]
+    plan = plan_full_prefill([SequenceSpec(0, 0, T)], n)
+    cfg = rc.GqaConfig(hq, hkv, 128)
+    blocks = [[materialize_rank_block(plan, r, [t]) for r in range(n)] for t in dev]
+    outs = ring_pass_kv_prefill(plan, [RankKvCache(hkv, 128, capacity_tokens=T) for _ in range(n)], *blocks, cfg)
+    o_tok = unshard(plan, [p.output.data for p in outs])[0]
+    l_tok = unshard(plan, [p.lse for p in outs])[0]
+    q, k, v = (orc.blk_from_tokens(a, np.arange(T)) for a in arrs)
+    want_o, want_l = orc.gqa(q, k, v, hkv)
+    assert np.abs(o_tok.cpu().numpy() - want_o).max() <= G.O_TOL
+    assert G.lse_err(l_tok.cpu().numpy(), want_l) <= G.LSE_TOL
+
+
+def _bf16_exact(x):
+    from tests.golden.make_golden_inputs import bf16_exact
+
+    return bf16_exact(x)

@@ -5,6 +5,88 @@
 #include "attn_common.cuh"
 
 namespace rcp {
+// ---- CTA-pair (cta_group::2) primitives used by the v5 / v8 variants
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load whose completion is reported to the LEADER CTA's barrier (same smem offset).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint64_t* bar, int c0,
+                                                 int c1, uint64_t hint) {
+  const uint32_t b = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)),
+      "r"(b), "r"(c0), "r"(c1), "l"(hint)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_ss_lo(uint32_t d, uint32_t a_lo, uint32_t b_lo, uint32_t idesc,
+                                           uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\n.reg .b64 da, db;\nsetp.ne.b32 p, %5, 0;\nmov.b64 da, {%1, %3};\n"
+      "mov.b64 db, {%2, %3};\ntcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %4, p;\n}\n" ::"r"(d),
+      "r"(a_lo), "r"(b_lo), "n"(kSw128DescHi), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_ts_lo(uint32_t d, uint32_t a, uint32_t b_lo, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\n.reg .b64 db;\nsetp.ne.b32 p, %5, 0;\nmov.b64 db, {%2, %3};\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], db, %4, p;\n}\n" ::"r"(d),
+      "r"(a), "r"(b_lo), "n"(kSw128DescHi), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// Commit to the barrier at this smem offset in BOTH CTAs of the pair.
+__device__ __forceinline__ void commit2_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+// Remote arrive on the leader CTA's barrier.  Default .release.cta semantics
+// (as CUTLASS's ClusterBarrier::arrive): the consumer of P is the leader's
+// tcgen05.mma, ordered by tcgen05.fence::before_thread_sync on this side and
+// fence::after_thread_sync after the wait.  A .release.cluster arrive stalled
+// the arriving warp ~1000 cycles per block (tools/trace_attn.py, v5).
+#ifndef RCP_ARRIVE_CLUSTER_RELEASE
+#define RCP_ARRIVE_CLUSTER_RELEASE 0
+#endif
+__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
+#if RCP_ARRIVE_CLUSTER_RELEASE
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & 0xFEFFFFFFu)
+               : "memory");
+#else
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & 0xFEFFFFFFu) : "memory");
+#endif
+}
+
+
+
+// Key-block rows of the round-1 variants (5-11).
+inline int attn_key_rows_r1(int version) { return (version == 7 || version >= 9) ? 64 : 128; }
+inline int attn_k_box_rows(int version) { return version == 6 ? 128 : 64; }
+inline int attn_v_box_rows(int version) { return (version == 7 || version >= 9) ? 64 : 128; }
+int attn_variant_launch(int version, const AttnParams& prm, int64_t n_pairs_heads, cudaStream_t st);
+}  // namespace rcp
+
+
+namespace rcp {
 
 // ======================================================================
 // v6: 1-CTA, 128-key blocks (default).  Same warp roles as v4, but S = Q K^T
