@@ -123,6 +123,14 @@ int rcp_decode_attn(const void* q, const void* k, const void* v, int64_t kv_row_
                     int64_t max_kv_len, int32_t hq, int32_t hkv, int32_t head_dim, float scale,
                     float* o, float* lse, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Decode-graph helper: copy row *counter of the device int64 table
+ * [n_rows, row_elems] to dst, then increment *counter (device int64, clamped
+ * at n_rows - 1).  GraphedDecode precomputes the per-step metadata of all of
+ * a graph's future steps (cache rows to append to, per-query KV segments,
+ * positions) and replays without any host->device upload per step. */
+int rcp_step_select(int64_t* dst, const int64_t* table, int64_t row_elems, int64_t* counter, int64_t n_rows,
+                    void* stream);
+
 /* Peer memory for the fused pass-Q All2All (Alg. 3's partial return,
  * SPEC.md:249-257): instead of an All2All after the ring, each ring step's
  * attention writes its partial O / LSE straight into the owning rank's

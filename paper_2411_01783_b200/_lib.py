@@ -52,6 +52,7 @@ SIGNATURES = {
         _c_void_p, ctypes.POINTER(_c_void_p), ctypes.POINTER(_i64), ctypes.POINTER(_i64),
         ctypes.POINTER(_i64), _i32, _i32, _i32, _i64, _c_void_p, _c_void_p, _i32, _c_void_p]),
     "rcp_gather_rows": (ctypes.c_int, [_c_void_p, _c_void_p, _c_void_p, _i64, _i64, _c_void_p]),
+    "rcp_step_select": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, _c_void_p, _i64, _c_void_p]),
     "rcp_shard_scatter": (ctypes.c_int, [
         ctypes.POINTER(_c_void_p), _c_void_p, ctypes.POINTER(_i64), _i32, _i32, _i32, _i64, _c_void_p]),
     "rcp_fold_meta": (ctypes.c_int, [

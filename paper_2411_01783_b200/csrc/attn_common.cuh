@@ -59,6 +59,7 @@ struct AttnParams {
   int64_t q_stride;        // elements between consecutive query rows
   long long* trace;  // RCP_TRACE builds only: per-CTA role timestamps (clock64)
   int* item_ctr;     // v9: work-item counter (workspace, zeroed by active_list_kernel)
+  int mask_shift;    // negative-control hook (RCP_FAULT=mask_diag): 1 excludes key == query; else 0
 };
 
 #ifndef RCP_TRACE

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(256) active_list_kernel(const TileSum* __restr
                                                           const TileSum* __restrict__ k_sum,
                                                           int n_qtiles, int n_kblocks,
                                                           uint32_t* __restrict__ act,
-                                                          int* __restrict__ act_n) {
+                                                          int* __restrict__ act_n, int drop_last) {
   __shared__ int warp_cnt[8];
   __shared__ int base;
   const int qb = blockIdx.x;
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) active_list_kernel(const TileSum* __restr
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) act_n[qb] = base;
+  if (threadIdx.x == 0) act_n[qb] = (drop_last && base > 0) ? base - 1 : base;  // drop_last: negative control
   if (qb == 0 && threadIdx.x == 0) act_n[gridDim.x] = 0;  // v9's work-item counter (workspace slack)
 }
 
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     const int t = static_cast<int>(threadIdx.x) - 128 - 128 * w;  // row inside the tile
     const int row = (2 * qblk + w) * kQRows + t;
     const bool row_ok = row < p.tq;
-    const int my_pos = row_ok ? __ldg(p.q_pos + row) : -1;
+    const int my_pos = row_ok ? __ldg(p.q_pos + row) - p.mask_shift : -1;
     const int my_seq = row_ok ? __ldg(p.q_seq + row) : RCP_SEQ_PAD_Q;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     const uint32_t o_addr = lane_base + kTmemO + w * kD;
@@ -506,6 +506,20 @@ extern "C" void rcp_debug_hang_info(int* out) {
 }
 #endif
 
+int rcp::rcp_fault_flags() {
+  static int flags = -1;
+  if (flags < 0) {
+    const char* e = getenv("RCP_FAULT");
+    flags = 0;
+    if (e) {
+      if (strstr(e, "drop_block")) flags |= kFaultDropBlock;
+      if (strstr(e, "mask_diag")) flags |= kFaultMaskDiag;
+      if (strstr(e, "reverse_merge")) flags |= kFaultReverseMerge;
+    }
+  }
+  return flags;
+}
+
 // Workspace: tile summaries | active lists (n_qblk x n_kblocks) | list lengths.
 extern "C" size_t rcp_attn_workspace_bytes(int64_t tq, int64_t tk) {
   const int64_t nq = (tq + kQRows - 1) / kQRows, nk = (tk + kKRows - 1) / kKRows;
@@ -581,7 +595,9 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
   uint32_t* act = reinterpret_cast<uint32_t*>(ksum + n_kblocks);
   const int n_qblk = (n_qtiles + 1) / 2;
   int* act_n = reinterpret_cast<int*>(act + static_cast<int64_t>(n_qblk) * n_kblocks);
-  active_list_kernel<<<n_qblk, 256, 0, st>>>(qsum, ksum, n_qtiles, n_kblocks, act, act_n);
+  const int fault = rcp_fault_flags();
+  active_list_kernel<<<n_qblk, 256, 0, st>>>(qsum, ksum, n_qtiles, n_kblocks, act, act_n,
+                                             (fault & kFaultDropBlock) ? 1 : 0);
   RCP_CUDA(cudaGetLastError());
   prm.act = act;
   prm.act_n = act_n;
@@ -604,6 +620,7 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
   prm.n_kblocks = n_kblocks;
   prm.mode = mode;
   prm.scale_log2 = static_cast<float>(static_cast<double>(scale) * 1.4426950408889634);
+  prm.mask_shift = (fault & kFaultMaskDiag) ? 1 : 0;
   prm.trace = g_trace;
 
   const int64_t grid = static_cast<int64_t>(prm.n_qblk) * hq;

@@ -99,7 +99,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
   // Registers: the softmax rows hold 128 scores; the TMA / MMA / TMEM warpgroup
-  // needs few.  65536 = 128 x 56 + 256 x 224 (setmaxnreg at the head of each
+  // needs few.  128 x 56 + 256 x 224 = 64512 = the launch allocation 384 x 168
+  // (.inc can only take what .dec released; setmaxnreg at the head of each
   // warpgroup's branch, so every role's code sits under one register limit).
   if (warp < 4) {
    setmaxnreg_dec<56>();
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid
     const int t = static_cast<int>(threadIdx.x) - 128 - 128 * w;  // row inside the tile
     const int row = (2 * qblk + w) * kQRows + t;
     const bool row_ok = row < p.tq;
-    const int my_pos = row_ok ? __ldg(p.q_pos + row) : -1;
+    const int my_pos = row_ok ? __ldg(p.q_pos + row) - p.mask_shift : -1;
     const int my_seq = row_ok ? __ldg(p.q_seq + row) : RCP_SEQ_PAD_Q;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     const uint32_t o_addr = lane_base + kTmemO + w * kD;

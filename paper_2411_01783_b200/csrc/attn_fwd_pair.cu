@@ -61,7 +61,7 @@ constexpr int kKRowsP = 128;                 // keys per block
 constexpr int kSlotsP = 11;                  // 16 KB half-block slots (K half, V half, ...)
 constexpr uint32_t kSlotBytesP = 16384;      // K half: 64 keys x 128 dims; V half: 128 keys x 64 dims
 constexpr uint32_t kSmemBytesP = kQTileBytes + kSlotsP * kSlotBytesP + 1024;
-static_assert(kSmemBytesP + 4096 <= 232448, "v13 shared memory (+ static barriers / exchange arrays) exceeds 227 KB");
+static_assert(kSmemBytesP + 8192 <= 232448, "v13 shared memory (+ static barriers / exchange arrays) exceeds 227 KB");
 constexpr uint32_t kTmemOP = 0, kTmemSP = 128;
 #ifndef RCP_POLY_PAIRS_P
 #define RCP_POLY_PAIRS_P 2
@@ -138,8 +138,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   __shared__ uint64_t bar_q, bar_full[kSlotsP], bar_empty[kSlotsP];
   __shared__ uint64_t bar_s[kSBufP], bar_p[kSBufP], bar_pv[2], bar_o;
   __shared__ uint32_t tmem_slot;
-  __shared__ float m_xch[2][128];  // [producing group][row]: running max handed to the other group
-  __shared__ float l_xch[2][128];  // epilogue: each group's (m, l)
+  __shared__ float m_xch[2][128];  // [producing group][row]: m(it) handed to the other group
+  __shared__ float l_xch[2][128];  // epilogue: each group's row sum
 
   const int warp = static_cast<int>(warp_id());
   // Pair order as v4: KV-head major, heavy (late) query blocks first, then the
@@ -182,8 +182,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_arrive_wait();
   tc_fence_after();
 
+  // Registers: the softmax rows hold 128 scores, the TMA / MMA / TMEM
+  // warpgroup needs few.  setmaxnreg.inc can only take what .dec released
+  // from the launch allocation (384 x 168 = 64512, not the 65536 of the
+  // file: 128 x 32 + 256 x 240 hangs the increase), so 128 x 40 + 256 x 232.
   if (warp < 4) {
-    setmaxnreg_dec<32>();
+    setmaxnreg_dec<40>();
     int rank, qblk, head, kvh, n;
     const uint32_t* act;
     coords(rank, qblk, head, kvh, n, act);
@@ -284,7 +288,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       __syncwarp();
     }
   } else {
-    setmaxnreg_inc<240>();
+    setmaxnreg_inc<232>();
     int rank, qblk, head, kvh, n;
     const uint32_t* act;
     coords(rank, qblk, head, kvh, n, act);
@@ -295,14 +299,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int q4 = warp & 3;                                      // TMEM lane quarter / SMSP
     const int row = (2 * qblk + rank) * kQRows + t;
     const bool row_ok = row < p.tq;
-    const int my_pos = row_ok ? __ldg(p.q_pos + row) : -1;
+    const int my_pos = row_ok ? __ldg(p.q_pos + row) - p.mask_shift : -1;
     const int my_seq = row_ok ? __ldg(p.q_seq + row) : RCP_SEQ_PAD_Q;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
     const uint32_t o_addr = lane_base + kTmemOP;
     const float sl2 = p.scale_log2;
     const uint64_t sl2x2 = f2(sl2, sl2);
-    // Named barriers 1..8: (quarter, direction) — group 0 -> 1 is 1 + q4, group 1 -> 0 is 5 + q4;
-    // 64 threads = the two warps of this lane quarter.
+    // Named barriers (64 threads = the two warps of this lane quarter):
+    // 1 + q4 + 4 g hands m from group g to the other group; 9 + q4 is the
+    // epilogue's.
     const uint32_t bar_give = 1 + q4 + 4 * g, bar_take = 1 + q4 + 4 * (g ^ 1);
     float m = -INFINITY;   // m (log2 units) after the last block this group processed
     float mg = -INFINITY;  // the m this group's row sum lg is expressed in
@@ -352,13 +357,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&bar_s[buf], (it / kSBufP) & 1);
       tc_fence_after();
       if (t == 0) TRACE(2 + 2 * g, it >> 1);
-      // Exp phases alternate between the two groups (per SMSP: the two warps of
-      // this lane quarter): group g takes m(it-1) from the other group only once
-      // that group's exps of block it-1 are done, and hands m(it) on right
-      // after its own.  One warp at a time drives the SMSP's MUFU / FMA pipes
-      // while the other loads S / reduces its max / publishes; the running
-      // max is exact (no speculation) and the S triple buffer keeps the
-      // tensor cores fed while a group waits for its turn.
+      // The running max m(it) = lazy(m(it-1), max of block it) chains the
+      // blocks of both groups: group g takes m(it-1) from the other group and
+      // hands m(it) on.  The exps run first, with the provisional m of the
+      // group's own chain, so they never wait; the exact m(it) is settled after
+      // them, and in the rare case it differs (the other group raised m at
+      // it-1) this row's P and block sum are rescaled by the exact power of two.
       uint32_t s[128];  // scores (fp32 bits) of this row
       float mx = -INFINITY;
       if (cls != kTileEmpty) {  // uniform across the CTA
@@ -383,34 +387,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
       }
       if (t == 0 && g == 0) TRACE(8, it >> 1);
-      // turn + running max after block it-1
-      const float m_in = it > 0 ? (named_bar_sync(bar_take, 64), m_xch[g ^ 1][t]) : -INFINITY;
-      const float m_fin = lazy_max(m_in, mx * sl2);
-      // O rescale when block it raised m over a non-empty O: after PV(it-1)
-      // completed (PV(it) waits for this group's P)
-      const bool raised = m_fin != m_in && m_in != -INFINITY;
-      if (__any_sync(0xffffffffu, raised)) {
-        const float f = raised ? ex2_approx(m_in - m_fin) : 1.0f;
-        // PV(it-1) is phase (it-1)/2 of bar_pv[(it-1)&1]; PV(it-3) (same barrier,
-        // one phase earlier) completed before S(it) was issued and PV(it+1)
-        // cannot start before this group's P(it), so the parity is unambiguous
-        mbar_wait(&bar_pv[(it - 1) & 1], ((it - 1) >> 1) & 1);
-        tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < kD; c += 8) {  // small chunks: the 128 scores are live here
-          uint32_t r[8];
-          tmem_ld8(o_addr + c, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 8; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
-          tmem_st8(o_addr + c, r);
-        }
-        tmem_st_wait();
-      }
-      if (t == 0 && g == 0) TRACE(9, it >> 1);
+      const float mx_l2 = mx * sl2;
+      // provisional m of this block from this group's own chain (m holds m(it-2)):
+      // the exps never wait for the other group
+      const float m_prov = lazy_max(m, mx_l2);  // m: this group's m after its previous block
       float bsum = 0.f;
       if (cls != kTileEmpty) {
-        const float m_use = (m_fin == -INFINITY) ? 0.f : m_fin;
+        const float m_use = (m_prov == -INFINITY) ? 0.f : m_prov;
         const uint64_t negm2 = f2(-m_use, -m_use);
         uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
         auto exp_chunks = [&](auto full) {
@@ -452,10 +435,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tmem_st32(s_addr, pk);
         tmem_st32(s_addr + 32, pk);
       }
-      // hand the turn and m(it) to the other group
+      if (t == 0 && g == 0) TRACE(9, it >> 1);
+      // settle m(it): take m(it-1) from the other group, hand m(it) on
+      const float m_in = it > 0 ? (named_bar_sync(bar_take, 64), m_xch[g ^ 1][t]) : -INFINITY;
+      const float m_fin = lazy_max(m_in, mx_l2);
       if (it + 1 < n) {
         m_xch[g][t] = m_fin;
         named_bar_arrive(bar_give, 64);
+      }
+      if (t == 0 && g == 0) TRACE(10, it >> 1);
+      // rare: P was made with a different m (the other group raised m at it-1)
+      // -> rescale this row's P and block sum by the exact power of two
+      const bool fix_p = m_prov != m_fin && m_prov != -INFINITY && cls != kTileEmpty;
+      if (__any_sync(0xffffffffu, fix_p)) {
+        const float fp = fix_p ? ex2_approx(m_prov - m_fin) : 1.0f;
+        tmem_st_wait();
+#pragma unroll 1
+        for (int c = 0; c < 64; c += 8) {
+          uint32_t pk[8];
+          tmem_ld8(s_addr + c, pk);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float2 v2 = unpack_bf16x2(pk[i]);
+            pk[i] = pack_bf16x2(v2.x * fp, v2.y * fp);
+          }
+          tmem_st8(s_addr + c, pk);
+        }
+        bsum *= fp;
+      }
+      // O rescale when block it raised m over a non-empty O: after PV(it-1)
+      // completed (PV(it) waits for this group's P)
+      const bool raised = m_fin != m_in && m_in != -INFINITY;
+      if (__any_sync(0xffffffffu, raised)) {
+        const float f = raised ? ex2_approx(m_in - m_fin) : 1.0f;
+        // PV(it-1) is phase (it-1)/2 of bar_pv[(it-1)&1]; PV(it-3) (same barrier,
+        // one phase earlier) completed before S(it) was issued and PV(it+1)
+        // cannot start before this group's P(it), so the parity is unambiguous
+        mbar_wait(&bar_pv[(it - 1) & 1], ((it - 1) >> 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < kD; c += 8) {
+          uint32_t r[8];
+          tmem_ld8(o_addr + c, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
+          tmem_st8(o_addr + c, r);
+        }
       }
       m = m_fin;
       // this group's row sum, in units of the current m
@@ -466,7 +493,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       lg += bsum;
       tmem_st_wait();
       tc_fence_before();
-      if (t == 0 && g == 0) TRACE(10, it >> 1);
       __syncwarp();
       if ((threadIdx.x & 31) == 0) arrive_on_leader(&bar_p[buf]);
       if (t == 0) TRACE(3 + 2 * g, it >> 1);

@@ -287,6 +287,21 @@ __global__ void shard_scatter_kernel(const __grid_constant__ ShardArgs a, int32_
   }
 }
 
+// Row `*counter` of a [n_rows, row_elems] int64 table -> dst, then ++*counter
+// (clamped at n_rows - 1).  One CTA; lets a replayed CUDA graph step through
+// metadata precomputed for all of its future steps without a host upload.
+__global__ void __launch_bounds__(256) step_select_kernel(int64_t* __restrict__ dst,
+                                                          const int64_t* __restrict__ table, int64_t row_elems,
+                                                          int64_t* __restrict__ counter, int64_t n_rows) {
+  __shared__ int64_t c;
+  if (threadIdx.x == 0) c = *counter;
+  __syncthreads();
+  const int64_t r = c < n_rows ? c : n_rows - 1;
+  for (int64_t i = threadIdx.x; i < row_elems; i += blockDim.x) dst[i] = table[r * row_elems + i];
+  __syncthreads();
+  if (threadIdx.x == 0) *counter = c + 1;
+}
+
 static unsigned grid_for(int64_t work, int threads) {
   int64_t b = (work + threads - 1) / threads;
   const int64_t cap = 148 * 16;
@@ -336,12 +351,14 @@ int rcp_merge_attn(const float* const* o_parts, const float* const* lse_parts, i
   if (rows == 0) return RCP_OK;
   MergeArgs a;
   memset(&a, 0, sizeof(a));
+  const bool reverse = (rcp_fault_flags() & kFaultReverseMerge) != 0;  // negative control only
   for (int i = 0; i < n; ++i) {
     RCP_CHECK_ARG(o_parts[i] && lse_parts[i], "null partial %d", i);
     RCP_CHECK_ARG((reinterpret_cast<uintptr_t>(o_parts[i]) & 15) == 0,
                   "partial %d output must be 16-byte aligned", i);
-    a.o[i] = o_parts[i];
-    a.lse[i] = lse_parts[i];
+    const int k = reverse ? n - 1 - i : i;
+    a.o[k] = o_parts[i];
+    a.lse[k] = lse_parts[i];
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (head_dim == 128 && n >= 2 && n <= 8) {
@@ -439,6 +456,15 @@ int rcp_shard_scatter(void* const* dst_rows, const void* src, const int64_t* new
   const int64_t vpr = row_bytes / 16;
   shard_scatter_kernel<<<grid_for(slot * 32, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       a, n_seqs, n_ranks, rank, vpr, static_cast<const uint4*>(src));
+  RCP_CUDA(cudaGetLastError());
+  return RCP_OK;
+}
+
+int rcp_step_select(int64_t* dst, const int64_t* table, int64_t row_elems, int64_t* counter, int64_t n_rows,
+                    void* stream) {
+  RCP_CHECK_ARG(dst && table && counter, "null pointer");
+  RCP_CHECK_ARG(row_elems >= 1 && n_rows >= 1, "bad sizes");
+  step_select_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(dst, table, row_elems, counter, n_rows);
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
 }

@@ -34,6 +34,12 @@ void set_error(const char* fmt, ...);
     }                                                                               \
   } while (0)
 
+// Negative-control hooks for the parity harness (tests/test_gpu_negative_controls.py):
+// RCP_FAULT=drop_block | mask_diag | reverse_merge makes the library WRONG on
+// purpose (read once per process; never set in production).
+enum : int { kFaultNone = 0, kFaultDropBlock = 1, kFaultMaskDiag = 2, kFaultReverseMerge = 4 };
+int rcp_fault_flags();
+
 // ------------------------------------------------------------------ merge math
 // One pairwise LSE merge step, the fp32 restatement of
 // ringcp.attention._merge_pair (attention.py:299-316).  Written with explicit

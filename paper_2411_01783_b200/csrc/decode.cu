@@ -346,9 +346,14 @@ __global__ void __launch_bounds__(kCombineWarps * 32) decode_combine_kernel(
 #ifndef RCP_DEC_CTA_TARGET
 #define RCP_DEC_CTA_TARGET (148 * 8)
 #endif
+// Batch rows counted by the split heuristic: the all-gathered decode form
+// launches N x slots query rows of which, at small batch, only ~1/N are
+// active (the rest are empty slots with kv_len 0), so sizing the split by the
+// full row count left the active rows with ~2 CTAs per SM at B = 1 (cfg5).
+static int64_t split_rows(int64_t batch) { return batch <= 4 ? 1 : (batch + 3) / 4; }
 static int keys_per_cta(int64_t batch, int32_t hkv, int64_t max_kv_len) {
   const int64_t target = RCP_DEC_CTA_TARGET;
-  int64_t per = (max_kv_len * batch * hkv + target - 1) / target;
+  int64_t per = (max_kv_len * split_rows(batch) * hkv + target - 1) / target;
   per = (per + kDecBlock - 1) / kDecBlock * kDecBlock;
   if (per < 8 * kDecBlock) per = 8 * kDecBlock;
   return static_cast<int>(per);

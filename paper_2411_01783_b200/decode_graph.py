@@ -55,7 +55,7 @@ class GraphedDecode:
     """
 
     def __init__(self, comm, cache: RankKvCache, cfg: GqaConfig, batch, max_steps: int = 256,
-                 first_iteration: int = 0):
+                 first_iteration: int = 0, first_positions=None):
         if cache.device.type != "cuda":
             raise RuntimeError("GraphedDecode needs the cache on a CUDA device")
         self.comm, self.cache, self.cfg = comm, cache, cfg
@@ -96,6 +96,16 @@ class GraphedDecode:
         self.graph = None
         self._arena_ptr = None
         self._segs_at_capture = None
+        # Device-resident step metadata: with the sequences' next global
+        # positions known (every sequence decodes one token per step), the
+        # metadata of every future step is precomputed once and the graph's
+        # first launch selects the current row (rcp_step_select) — no
+        # host->device upload and no metadata work on the host per step.
+        self._table = None
+        self._pos_next = None
+        if first_positions is not None:
+            self._pos_next = {int(sid): int(first_positions[sid]) for sid in self.batch}
+            self._build_table()
 
     def _segment_key(self):
         """(start, capacity) of every batch sequence's arena segment: the
@@ -111,9 +121,45 @@ class GraphedDecode:
         if self.ws.numel() < need:
             self.ws = torch.empty(need, dtype=torch.uint8, device=self.cache.device)
 
+    def _build_table(self) -> None:
+        """Metadata rows (rows | starts | lens | pos | seq) of steps self.it ..
+        self.it + steps_left - 1, simulated from the current segments."""
+        c, S, n = self.cache, self.slots, self.n
+        steps = max(self.steps_left, 1)
+        sim = {sid: [c._segs[sid].start, c._segs[sid].length, c._segs[sid].cap] for sid in self.batch}
+        pos = dict(self._pos_next)
+        table = np.empty((steps, self.meta.numel()), np.int64)
+        for k in range(steps):
+            plan = plan_decode(self.batch, n, self.it + k)
+            rows = np.full(S, self.scratch_row, np.int64)
+            pos32 = np.full(S, _lib.POS_PAD_K, np.int64)
+            seq32 = np.full(S, _lib.SEQ_PAD_K, np.int64)
+            for j, (sid, _b) in enumerate(plan.assignments[self.rank]):
+                seg = sim[sid]
+                if seg[1] >= seg[2]:
+                    raise RuntimeError("GraphedDecode: reservation too small for max_steps")
+                rows[j] = seg[0] + seg[1]
+                seg[1] += 1
+                pos32[j], seq32[j] = pos[sid], sid
+            starts = np.zeros(n * S, np.int64)
+            lens = np.zeros(n * S, np.int64)
+            for src in range(n):
+                for j, (sid, _b) in enumerate(plan.assignments[src]):
+                    starts[src * S + j], lens[src * S + j] = sim[sid][0], sim[sid][1]
+            for sid in self.batch:
+                pos[sid] += 1
+            table[k] = np.concatenate([rows, starts, lens, pos32, seq32])
+        self._table = torch.from_numpy(table).to(self.cache.device)
+        self._table_first_it = self.it
+        self._counter = torch.zeros(1, dtype=torch.int64, device=self.cache.device)
+
     # ------------------------------------------------------------------ launches
     def _launches(self):
         c, S = self.cache, self.slots
+        if self._table is not None:
+            _lib.check(_lib.load().rcp_step_select(
+                _lib.ptr(self.meta), _lib.ptr(self._table), self.meta.numel(), _lib.ptr(self._counter),
+                self._table.shape[0], _lib.stream_handle()))
         rows = self.meta[:S]
         c.k.index_copy_(0, rows, self.k_in)
         c.v.index_copy_(0, rows, self.v_in)
@@ -181,15 +227,31 @@ class GraphedDecode:
             self.q_in[:m].copy_(q_tok[:m])
             self.k_in[:m].copy_(k_tok[:m])
             self.v_in[:m].copy_(v_tok[:m])
-        meta = self._host_meta(mine, positions)
-        _lib.h2d(meta, self.cache.device, out=self.meta)  # ordered after the previous replay
+        if self._table is not None and (
+                any(int(positions[j]) != self._pos_next[sid] for j, (sid, _b) in enumerate(mine))
+                or (self.graph is not None and self._segment_key() != self._segs_at_capture)):
+            # not the consecutive positions / unmoved segments the table assumed:
+            # back to per-step metadata uploads (re-captured without the selector)
+            self._table = None
+            self.graph = None
+        if self._table is not None:
+            meta = None
+            for j, (sid, _b) in enumerate(mine):  # host bookkeeping of this step's appends
+                seg = self.cache._segs[sid]
+                seg.length += 1
+                seg.max_pos = int(positions[j])
+            for sid in self.batch:
+                self._pos_next[sid] += 1
+        else:
+            if self.graph is not None and self._segment_key() != self._segs_at_capture:
+                self._refit()  # a segment moved / grew since capture: the baked split bound is stale
+                self.graph = None
+            meta = self._host_meta(mine, positions)
+            if max(int(x) for x in meta[_lens_slice(self)]) > self.max_len:
+                raise RuntimeError("GraphedDecode: a KV segment exceeds the captured split bound")
+            _lib.h2d(meta, self.cache.device, out=self.meta)  # ordered after the previous replay
         ptrs = (self.cache.k.data_ptr(), self.cache.v.data_ptr(), self.cache.pos.data_ptr(),
                 self.cache.seq.data_ptr())
-        if self.graph is not None and self._segment_key() != self._segs_at_capture:
-            self._refit()  # a segment moved / grew since capture: the baked split bound is stale
-            self.graph = None
-        if max(int(x) for x in meta[_lens_slice(self)]) > self.max_len:
-            raise RuntimeError("GraphedDecode: a KV segment exceeds the captured split bound")
         if self.graph is None or ptrs != self._arena_ptr:
             # the warm-up launch in _capture executes this step (capture only
             # records), so the step's appends and outputs happen exactly once

@@ -14,8 +14,11 @@ from oracle import ringcp_oracle as orc
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("hist", [(3000, 1500), (700, 2)])
-def test_graphed_decode_matches_oracle(hist):
+@pytest.mark.parametrize("hist,table", [((3000, 1500), False), ((700, 2), False), ((3000, 1500), True),
+                                        ((700, 2), True)])
+def test_graphed_decode_matches_oracle(hist, table):
+    """table=True: the step metadata of all future steps is precomputed on the
+    device (first_positions given) and selected by the graph itself."""
     from paper_2411_01783_b200.attention import GqaConfig
     from paper_2411_01783_b200.decode_graph import GraphedDecode
     from paper_2411_01783_b200.kv_cache import RankKvCache
@@ -32,7 +35,9 @@ def test_graphed_decode_matches_oracle(hist):
         k, v = bf(L, hkv, D), bf(L, hkv, D)
         cache.append_rows(sid, k.cuda(), v.cuda(), np.arange(L))
         host[sid] = [k.float().numpy(), v.float().numpy()]
-    g = GraphedDecode(_LocalComm(0, 1), cache, cfg, batch, max_steps=8)
+    first = {sid: L for sid, L in zip(batch, hist)} if table else None
+    g = GraphedDecode(_LocalComm(0, 1), cache, cfg, batch, max_steps=8, first_positions=first)
+    assert (g._table is not None) == table
     for step in range(6):
         q, k, v = bf(2, hq, D), bf(2, hkv, D), bf(2, hkv, D)
         pos = [cache.cached_len(s) for s in batch]
@@ -48,6 +53,7 @@ def test_graphed_decode_matches_oracle(hist):
             assert np.abs(out[j] - o_w[0]).max() < 2e-2, (step, sid)
             assert np.abs(lse[j] - l_w[0]).max() < 1e-3, (step, sid)
         assert g.graph is not None  # captured on the first step, replayed afterwards
+        assert (g._table is not None) == table  # consecutive positions keep the device table
     assert [cache.cached_len(s) for s in batch] == [hist[0] + 6, hist[1] + 6]
     # the cached rows are the appended tokens, in position order
     for sid in batch:

@@ -103,7 +103,9 @@ def test_cross_sequence_keys_are_never_admitted(rc):
     k_other = make_block(rc, rng, 4, 2, 4, seq_id=2)
     _, lse = np_out(rc.gqa_attention(q, k_other, k_other, cfg))
     assert np.all(np.isneginf(lse))
-    assert rc.admitted_pair_count(q, k_other) == 0
+    from paper_2411_01783_b200.attention import admitted_pair_count
+
+    assert admitted_pair_count(q, k_other) == 0
 
 
 def test_padding_rows_change_nothing_bitwise(rc):
@@ -297,12 +299,14 @@ def test_block_split_invariance(seed, n_keys, n_blocks, n_kv_heads):
 # ------------------------------------------------------------------ API surface not covered above
 def test_admitted_pair_count_matches_reference_golden(rc):
     """admitted_pair_count (attention.py:209-211) on device vs the reference's own counts."""
+    from paper_2411_01783_b200.attention import admitted_pair_count
+
     z = G.npz("gqa.npz")
     for name in z["names"]:
         c = G.gqa_case(z, name)
         q = rc.EmbeddingBlock(c["q"].data, c["q"].pos, c["q"].valid, c["q"].seq)
         k = rc.EmbeddingBlock(c["k"].data, c["k"].pos, c["k"].valid, c["k"].seq)
-        assert rc.admitted_pair_count(q, k) == c["pairs"], name
+        assert admitted_pair_count(q, k) == c["pairs"], name
 
 
 @pytest.mark.parametrize("data,pos,valid,seq,msg", [

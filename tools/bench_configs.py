@@ -182,8 +182,11 @@ def run_decode(args, rank, world):
             # growing by one token per sequence per step, as in serving.
             from paper_2411_01783_b200.decode_graph import GraphedDecode
 
-            gd = GraphedDecode(comm, cache, cfg, batch, max_steps=args.warmup + args.steps + 2)
             pos0 = {b: max(lens[b], args.context) for b in batch}
+            # consecutive positions per step: the step metadata is precomputed on the
+            # device and selected by the graph (no per-step upload / host metadata)
+            gd = GraphedDecode(comm, cache, cfg, batch, max_steps=args.warmup + args.steps + 2,
+                               first_positions=None if args.no_table else pos0)
 
             def step():  # noqa: F811 - graphed variant
                 it = gd.it
@@ -198,7 +201,7 @@ def run_decode(args, rank, world):
             print(json.dumps({
                 "config": "cfg5-ring-pass-q-decode", "cp": world, "batch": B, "context": args.context,
                 "q_transport": "allgather" if (args.gather or args.graph) else "ring",
-                "cuda_graph": bool(args.graph),
+                "cuda_graph": bool(args.graph), "device_step_table": bool(args.graph and not args.no_table),
                 "n_q_heads": hq, "n_kv_heads": hkv, "step_ms": ms,
                 "kv_bytes_per_rank": kv_bytes, "hbm_gbs_effective": kv_bytes / (ms * 1e-3) / 1e9}), flush=True)
         del cache
@@ -215,6 +218,8 @@ def main():
     ap.add_argument("--batch", type=int, nargs="*", default=[1, 2, 4, 8, 16, 32])
     ap.add_argument("--gather", action="store_true", help="decode: all-gather Q instead of the Q ring")
     ap.add_argument("--graph", action="store_true", help="decode: replay the step from a CUDA graph")
+    ap.add_argument("--no-table", action="store_true",
+                    help="decode --graph: upload the step metadata each step instead of the device table")
     ap.add_argument("--fused", action="store_true",
                     help="partial: also time pass-Q with peer-memory partials (no All2All), checked bitwise")
     ap.add_argument("--steps", type=int, default=5)

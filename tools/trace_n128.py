@@ -64,7 +64,7 @@ if os.environ.get("RCP_ATTN_VERSION") == "13":
             print(f"  group {gg}: softmax (S seen -> P arrive) {np.mean(p_arr - s_seen):.0f}; "
                   f"P arrive -> next own S seen {np.mean(s_seen[1:] - p_arr[:-1]):.0f}")
         g0 = d[4:28]
-        print(f"  group 0 phases: ld+max {np.mean(g0[:, 8] - g0[:, 2]):.0f}, turn wait+rescale {np.mean(g0[:, 9] - g0[:, 8]):.0f}, "
-              f"exp+st {np.mean(g0[:, 10] - g0[:, 9]):.0f}, tail {np.mean(g0[:, 3] - g0[:, 10]):.0f}")
+        print(f"  group 0 phases: ld+max {np.mean(g0[:, 8] - g0[:, 2]):.0f}, exps {np.mean(g0[:, 9] - g0[:, 8]):.0f}, "
+              f"handoff wait {np.mean(g0[:, 10] - g0[:, 9]):.0f}, fixups+tail {np.mean(g0[:, 3] - g0[:, 10]):.0f}")
         its = np.arange(8, 56, 2)
         print(f"  leader: P0(it) arrive -> PV(it) issued {np.mean(d[its, 0] - d[its // 2, 3]):.0f}")
