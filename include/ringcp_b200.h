@@ -131,6 +131,18 @@ int rcp_decode_attn(const void* q, const void* k, const void* v, int64_t kv_row_
 int rcp_step_select(int64_t* dst, const int64_t* table, int64_t row_elems, int64_t* counter, int64_t n_rows,
                     void* stream);
 
+/* Growable device arenas for the per-rank KV cache (RankKvCache):
+ * reserve a virtual address range once, then map physical memory into it in
+ * granularity-sized chunks as the cache grows — no copy of the cached rows and
+ * no old + new arena at once; the base pointer never moves (CUDA graphs and
+ * tensor maps stay valid).  rcp_vmm_map returns an opaque handle for
+ * rcp_vmm_unmap; rcp_vmm_free releases the (fully unmapped) range. */
+int rcp_vmm_granularity(int device, size_t* bytes_out);
+int rcp_vmm_reserve(size_t bytes, void** base_out);
+int rcp_vmm_map(void* base, size_t offset, size_t bytes, int device, uint64_t* handle_out);
+int rcp_vmm_unmap(void* base, size_t offset, size_t bytes, uint64_t handle);
+int rcp_vmm_free(void* base, size_t bytes);
+
 /* Peer memory for the fused pass-Q All2All (Alg. 3's partial return,
  * SPEC.md:249-257): instead of an All2All after the ring, each ring step's
  * attention writes its partial O / LSE straight into the owning rank's

@@ -52,6 +52,11 @@ SIGNATURES = {
         _c_void_p, ctypes.POINTER(_c_void_p), ctypes.POINTER(_i64), ctypes.POINTER(_i64),
         ctypes.POINTER(_i64), _i32, _i32, _i32, _i64, _c_void_p, _c_void_p, _i32, _c_void_p]),
     "rcp_gather_rows": (ctypes.c_int, [_c_void_p, _c_void_p, _c_void_p, _i64, _i64, _c_void_p]),
+    "rcp_vmm_granularity": (ctypes.c_int, [_i32, ctypes.POINTER(_size_t)]),
+    "rcp_vmm_reserve": (ctypes.c_int, [_size_t, ctypes.POINTER(_c_void_p)]),
+    "rcp_vmm_map": (ctypes.c_int, [_c_void_p, _size_t, _size_t, _i32, ctypes.POINTER(ctypes.c_uint64)]),
+    "rcp_vmm_unmap": (ctypes.c_int, [_c_void_p, _size_t, _size_t, ctypes.c_uint64]),
+    "rcp_vmm_free": (ctypes.c_int, [_c_void_p, _size_t]),
     "rcp_step_select": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, _c_void_p, _i64, _c_void_p]),
     "rcp_shard_scatter": (ctypes.c_int, [
         ctypes.POINTER(_c_void_p), _c_void_p, ctypes.POINTER(_i64), _i32, _i32, _i32, _i64, _c_void_p]),

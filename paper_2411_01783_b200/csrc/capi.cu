@@ -6,6 +6,9 @@
 #include <cstring>
 #include <string>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 
 namespace rcp {
@@ -508,3 +511,106 @@ extern "C" int rcp_ipc_close(void* dev_ptr) {
   return RCP_OK;
 }
 
+
+// ------------------------------------------------------------------ growable device arenas (CUDA VMM)
+// A KV-cache arena reserves one large virtual address range and maps physical
+// memory into it in granularity-sized chunks as it grows: growth never copies
+// the cached rows and never needs old + new arenas at once, and the arena's
+// base pointer (baked into CUDA graphs and tensor maps) never changes.
+namespace {
+template <typename F>
+F driver_fn(const char* name) {
+  void* f = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &f, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(f);
+}
+CUmemAllocationProp vmm_prop(int device) {
+  CUmemAllocationProp prop;
+  memset(&prop, 0, sizeof(prop));
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = device;
+  return prop;
+}
+}  // namespace
+
+#define RCP_CU(call)                                                        \
+  do {                                                                      \
+    CUresult r_ = (call);                                                   \
+    if (r_ != CUDA_SUCCESS) {                                               \
+      ::rcp::set_error("%s failed: CUresult %d", #call, static_cast<int>(r_)); \
+      return RCP_ERR_CUDA;                                                  \
+    }                                                                       \
+  } while (0)
+
+extern "C" int rcp_vmm_granularity(int device, size_t* bytes_out) {
+  RCP_CHECK_ARG(bytes_out != nullptr, "null pointer");
+  auto gran = driver_fn<PFN_cuMemGetAllocationGranularity_v10020>("cuMemGetAllocationGranularity");
+  RCP_CHECK_ARG(gran != nullptr, "CUDA VMM entry points unavailable");
+  CUmemAllocationProp prop = vmm_prop(device);
+  RCP_CU(gran(bytes_out, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+  return RCP_OK;
+}
+
+extern "C" int rcp_vmm_reserve(size_t bytes, void** base_out) {
+  RCP_CHECK_ARG(base_out != nullptr && bytes > 0, "bad arguments");
+  auto reserve = driver_fn<PFN_cuMemAddressReserve_v10020>("cuMemAddressReserve");
+  RCP_CHECK_ARG(reserve != nullptr, "CUDA VMM entry points unavailable");
+  CUdeviceptr p = 0;
+  RCP_CU(reserve(&p, bytes, 0, 0, 0));
+  *base_out = reinterpret_cast<void*>(p);
+  return RCP_OK;
+}
+
+// Map `bytes` (a multiple of the granularity) of new physical memory at base + offset.
+extern "C" int rcp_vmm_map(void* base, size_t offset, size_t bytes, int device, uint64_t* handle_out) {
+  RCP_CHECK_ARG(base != nullptr && bytes > 0 && handle_out != nullptr, "bad arguments");
+  auto create = driver_fn<PFN_cuMemCreate_v10020>("cuMemCreate");
+  auto map = driver_fn<PFN_cuMemMap_v10020>("cuMemMap");
+  auto access = driver_fn<PFN_cuMemSetAccess_v10020>("cuMemSetAccess");
+  auto release = driver_fn<PFN_cuMemRelease_v10020>("cuMemRelease");
+  auto unmap = driver_fn<PFN_cuMemUnmap_v10020>("cuMemUnmap");
+  RCP_CHECK_ARG(create && map && access && release && unmap, "CUDA VMM entry points unavailable");
+  CUmemAllocationProp prop = vmm_prop(device);
+  CUmemGenericAllocationHandle h;
+  RCP_CU(create(&h, bytes, &prop, 0));
+  const CUdeviceptr at = reinterpret_cast<CUdeviceptr>(base) + offset;
+  CUresult r = map(at, bytes, 0, h, 0);
+  if (r != CUDA_SUCCESS) {
+    release(h);
+    set_error("cuMemMap failed: CUresult %d", static_cast<int>(r));
+    return RCP_ERR_CUDA;
+  }
+  CUmemAccessDesc acc;
+  memset(&acc, 0, sizeof(acc));
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  r = access(at, bytes, &acc, 1);
+  if (r != CUDA_SUCCESS) {
+    unmap(at, bytes);
+    release(h);
+    set_error("cuMemSetAccess failed: CUresult %d", static_cast<int>(r));
+    return RCP_ERR_CUDA;
+  }
+  *handle_out = static_cast<uint64_t>(h);
+  return RCP_OK;
+}
+
+extern "C" int rcp_vmm_unmap(void* base, size_t offset, size_t bytes, uint64_t handle) {
+  auto unmap = driver_fn<PFN_cuMemUnmap_v10020>("cuMemUnmap");
+  auto release = driver_fn<PFN_cuMemRelease_v10020>("cuMemRelease");
+  RCP_CHECK_ARG(unmap && release, "CUDA VMM entry points unavailable");
+  RCP_CU(unmap(reinterpret_cast<CUdeviceptr>(base) + offset, bytes));
+  RCP_CU(release(static_cast<CUmemGenericAllocationHandle>(handle)));
+  return RCP_OK;
+}
+
+extern "C" int rcp_vmm_free(void* base, size_t bytes) {
+  auto free_fn = driver_fn<PFN_cuMemAddressFree_v10020>("cuMemAddressFree");
+  RCP_CHECK_ARG(free_fn != nullptr, "CUDA VMM entry points unavailable");
+  RCP_CU(free_fn(reinterpret_cast<CUdeviceptr>(base), bytes));
+  return RCP_OK;
+}

@@ -189,7 +189,7 @@ class GraphedDecode:
             self._launches()
         self.graph = g
         self._arena_ptr = (self.cache.k.data_ptr(), self.cache.v.data_ptr(), self.cache.pos.data_ptr(),
-                           self.cache.seq.data_ptr())
+                           self.cache.seq.data_ptr(), self.cache.k.shape[0])
         self._segs_at_capture = self._segment_key()
 
     # ------------------------------------------------------------------ per step
@@ -251,7 +251,7 @@ class GraphedDecode:
                 raise RuntimeError("GraphedDecode: a KV segment exceeds the captured split bound")
             _lib.h2d(meta, self.cache.device, out=self.meta)  # ordered after the previous replay
         ptrs = (self.cache.k.data_ptr(), self.cache.v.data_ptr(), self.cache.pos.data_ptr(),
-                self.cache.seq.data_ptr())
+                self.cache.seq.data_ptr(), self.cache.k.shape[0])  # (a grown VMM arena keeps its pointer)
         if self.graph is None or ptrs != self._arena_ptr:
             # the warm-up launch in _capture executes this step (capture only
             # records), so the step's appends and outputs happen exactly once

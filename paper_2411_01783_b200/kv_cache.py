@@ -12,6 +12,15 @@ message builder need.
 Position bookkeeping lives on the host (every append comes from a plan whose
 positions the host knows, or is checked once), so snapshots and ring messages
 are built without device synchronisation.
+
+Growth.  On a CUDA device the arenas are CUDA-VMM reservations (``_VmmArena``:
+one virtual range per array, physical memory mapped in as the cache grows), so
+growing the cache never copies the cached rows, never holds an old and a new
+arena at once, and never moves the base pointer that CUDA graphs and tensor
+maps hold.  A sequence whose segment is full moves to a larger segment (a copy
+of that sequence only, amortised by doubling); ``evict`` frees a sequence's
+segment for reuse (first fit).  ``capacity_balance`` checks the SPEC's
+decode capacity invariant over the ranks' caches.
 """
 
 from __future__ import annotations
@@ -24,7 +33,97 @@ import torch
 from . import _lib
 from .attention import EmbeddingBlock, _device
 
-__all__ = ["RankKvCache"]
+__all__ = ["RankKvCache", "capacity_balance"]
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of raw device memory (no ownership)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class _VmmArena:
+    """A growable device array [rows, *row_shape] backed by one CUDA VMM
+    virtual reservation (rcp_vmm_*): ``grow`` maps more physical memory after
+    the existing rows; the base address and the existing data never move."""
+
+    _TYPESTR = {torch.bfloat16: ("<i2", 2), torch.int32: ("<i4", 4), torch.float32: ("<f4", 4),
+                torch.int64: ("<i8", 8)}
+
+    def __init__(self, max_rows: int, row_shape, dtype, device: torch.device):
+        import ctypes
+
+        lib = _lib.load()
+        self.device = device
+        self.row_shape = tuple(row_shape)
+        self.dtype = dtype
+        self.typestr, self.elem = self._TYPESTR[dtype]
+        self.row_bytes = int(np.prod(self.row_shape, dtype=np.int64)) * self.elem if self.row_shape else self.elem
+        g = ctypes.c_size_t()
+        _lib.check(lib.rcp_vmm_granularity(device.index, ctypes.byref(g)))
+        self.gran = max(int(g.value), 2 << 20)
+        # K / V map in >= 64 MB steps; the 4-byte metadata arrays in granules
+        self.chunk = max(self.gran, 64 << 20) if self.row_bytes >= 64 else self.gran
+        self.reserved = -(-max(max_rows, 1) * self.row_bytes // self.gran) * self.gran
+        base = ctypes.c_void_p()
+        _lib.check(lib.rcp_vmm_reserve(self.reserved, ctypes.byref(base)))
+        self.base = int(base.value)
+        self.mapped = 0
+        self._maps = []  # (offset, bytes, handle)
+        self.rows = 0
+
+    def capacity_rows(self) -> int:
+        return self.mapped // self.row_bytes
+
+    def grow(self, rows: int) -> bool:
+        """Map memory for at least ``rows`` rows; True if memory was added."""
+        import ctypes
+
+        need = rows * self.row_bytes
+        if need <= self.mapped:
+            return False
+        if need > self.reserved:
+            raise RuntimeError(f"KV arena reservation exhausted ({self.reserved} bytes)")
+        add = max(-(-(need - self.mapped) // self.chunk) * self.chunk, self.mapped)  # at least double
+        add = min(add, self.reserved - self.mapped)
+        h = ctypes.c_uint64()
+        _lib.check(_lib.load().rcp_vmm_map(self.base, self.mapped, add, self.device.index, ctypes.byref(h)))
+        self._maps.append((self.mapped, add, int(h.value)))
+        self.mapped += add
+        return True
+
+    def tensor(self) -> torch.Tensor:
+        """The mapped rows as a tensor view (same base pointer every time)."""
+        rows = self.capacity_rows()
+        shape = (rows,) + self.row_shape
+        if self.dtype == torch.bfloat16:
+            t = torch.as_tensor(_CudaArray(self.base, shape, self.typestr), device=self.device)
+            return t.view(torch.bfloat16)
+        return torch.as_tensor(_CudaArray(self.base, shape, self.typestr), device=self.device)
+
+    def close(self) -> None:
+        lib = _lib.load()
+        torch.cuda.synchronize(self.device)
+        for off, nbytes, h in reversed(self._maps):
+            lib.rcp_vmm_unmap(self.base, off, nbytes, h)
+        self._maps = []
+        if self.base:
+            lib.rcp_vmm_free(self.base, self.reserved)
+        self.base = 0
+
+
+def capacity_balance(caches, seq_ids=None) -> dict:
+    """SPEC.md:200-203 invariants over the ranks' caches: per sequence the
+    cached rows summed over ranks (the Σ-invariant: every prefilled / decoded
+    token is cached exactly once), and the decode capacity balance — max over
+    ranks minus min over ranks of the rows a rank holds for the batch (after
+    k·N decode iterations of a B-sequence batch it is at most B)."""
+    ids = sorted(set(seq_ids) if seq_ids is not None else {s for c in caches for s in c.seq_ids()})
+    per_rank = [sum(c.cached_len(s) for s in ids) for c in caches]
+    return {"per_seq_total": {s: sum(c.cached_len(s) for c in caches) for s in ids},
+            "per_rank": per_rank, "spread": max(per_rank) - min(per_rank) if per_rank else 0}
 
 
 @dataclass
@@ -40,21 +139,62 @@ class RankKvCache:
     ``snapshot_padded(seq_id, max_len) -> (k_block, v_block)`` as in SPEC.md:180-198."""
 
     def __init__(self, n_kv_heads: int, head_dim: int, capacity_tokens: int = 1 << 16,
-                 dtype=torch.bfloat16, device=None):
+                 dtype=torch.bfloat16, device=None, growth: str | None = None, max_tokens: int | None = None):
+        """``growth``: "vmm" (default on CUDA: growable virtual arenas, no copy on
+        growth) or "copy" (reallocate by doubling; CPU tensors / tests).
+        ``max_tokens`` bounds the VMM reservation (default: what fits in the
+        device's memory)."""
         self.n_kv_heads = int(n_kv_heads)
         self.head_dim = int(head_dim)
         self.dtype = dtype
-        self.device = device if device is not None else _device()
+        self.device = torch.device(device) if device is not None else _device()
+        if self.device.type == "cuda" and self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self._cap = max(int(capacity_tokens), 1)
-        self.k = torch.zeros((self._cap, n_kv_heads, head_dim), dtype=dtype, device=self.device)
-        self.v = torch.zeros_like(self.k)
-        self.pos = torch.full((self._cap,), _lib.POS_PAD_K, dtype=torch.int32, device=self.device)
-        self.seq = torch.full((self._cap,), _lib.SEQ_PAD_K, dtype=torch.int32, device=self.device)
+        if growth is None:
+            growth = "vmm" if self.device.type == "cuda" else "copy"
+        self.growth = growth
+        self._free: list[tuple[int, int]] = []  # (start, cap) of evicted segments
         self._used = 0
         self._segs: dict[int, _Segment] = {}
+        if growth == "vmm":
+            row = self.n_kv_heads * self.head_dim * torch.tensor([], dtype=dtype).element_size()
+            if max_tokens is None:
+                total = torch.cuda.get_device_properties(self.device).total_memory
+                max_tokens = total // (2 * row)
+            max_tokens = max(int(max_tokens), self._cap)
+            self._arenas = {
+                "k": _VmmArena(max_tokens, (n_kv_heads, head_dim), dtype, self.device),
+                "v": _VmmArena(max_tokens, (n_kv_heads, head_dim), dtype, self.device),
+                "pos": _VmmArena(max_tokens, (), torch.int32, self.device),
+                "seq": _VmmArena(max_tokens, (), torch.int32, self.device),
+            }
+            self._cap = 0
+            self._grow_arena(max(int(capacity_tokens), 1))
+        else:
+            self._arenas = None
+            self.k = torch.zeros((self._cap, n_kv_heads, head_dim), dtype=dtype, device=self.device)
+            self.v = torch.zeros_like(self.k)
+            self.pos = torch.full((self._cap,), _lib.POS_PAD_K, dtype=torch.int32, device=self.device)
+            self.seq = torch.full((self._cap,), _lib.SEQ_PAD_K, dtype=torch.int32, device=self.device)
 
     # ---------------------------------------------------------------- storage
     def _grow_arena(self, need_rows: int):
+        if self._arenas is not None:
+            if need_rows <= self._cap:
+                return
+            old = self._cap
+            for a in self._arenas.values():
+                a.grow(need_rows)
+            self._cap = min(a.capacity_rows() for a in self._arenas.values())
+            self.k, self.v = self._arenas["k"].tensor(), self._arenas["v"].tensor()
+            self.pos, self.seq = self._arenas["pos"].tensor(), self._arenas["seq"].tensor()
+            # only the new rows are initialised; cached rows are neither copied nor moved
+            self.k[old:].zero_()
+            self.v[old:].zero_()
+            self.pos[old:].fill_(_lib.POS_PAD_K)
+            self.seq[old:].fill_(_lib.SEQ_PAD_K)
+            return
         new_cap = self._cap
         while new_cap < need_rows:
             new_cap *= 2
@@ -80,24 +220,78 @@ class RankKvCache:
         if seg.length + extra <= seg.cap:
             return seg
         new_cap = max(2 * seg.cap, seg.length + extra, 64)
-        if seg.start + seg.cap == self._used:  # last segment: grow in place
+        if seg.cap and seg.start + seg.cap == self._used:  # last segment: grow in place
             self._grow_arena(seg.start + new_cap)
             self._used = seg.start + new_cap
             seg.cap = new_cap
             return seg
-        start = self._used
-        self._grow_arena(start + new_cap)
+        start = self._take_free(new_cap)
+        if start is None:
+            start = self._used
+            self._grow_arena(start + new_cap)
+            self._used = start + new_cap
         if seg.length:
             for t in (self.k, self.v, self.pos, self.seq):
                 t[start:start + seg.length].copy_(t[seg.start:seg.start + seg.length])
+        if seg.cap:
+            self._release(seg.start, seg.cap)
         seg.start, seg.cap = start, new_cap
-        self._used = start + new_cap
         return seg
+
+    def _take_free(self, rows: int):
+        """First fit among evicted / vacated segments (the remainder stays free)."""
+        for i, (st, cap) in enumerate(self._free):
+            if cap >= rows:
+                if cap > rows:
+                    self._free[i] = (st + rows, cap - rows)
+                else:
+                    self._free.pop(i)
+                return st
+        return None
+
+    def _release(self, start: int, cap: int) -> None:
+        self._free.append((start, cap))
+        self._free.sort()
+        merged = []
+        for st, cp in self._free:  # coalesce neighbours
+            if merged and merged[-1][0] + merged[-1][1] == st:
+                merged[-1] = (merged[-1][0], merged[-1][1] + cp)
+            else:
+                merged.append((st, cp))
+        if merged and merged[-1][0] + merged[-1][1] == self._used:  # trailing space: shrink the used region
+            self._used = merged.pop()[0]
+        self._free = merged
+
+    def evict(self, seq_id: int) -> int:
+        """Drop a sequence from this rank's cache; its rows become reusable.
+        Returns the number of rows freed."""
+        seg = self._segs.pop(seq_id, None)
+        if seg is None:
+            return 0
+        if seg.cap:
+            self._release(seg.start, seg.cap)
+        return seg.length
+
+    def close(self) -> None:
+        """Release the device memory (VMM arenas: unmap and free the reservations
+        after the device has finished with them)."""
+        if getattr(self, "_arenas", None) is not None:
+            self.k = self.v = self.pos = self.seq = None
+            for a in self._arenas.values():
+                a.close()
+            self._arenas = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown / CUDA already torn down
+            pass
 
     def reset(self) -> None:
         """Forget every sequence (keeps the arena allocation)."""
         self._used = 0
         self._segs.clear()
+        self._free = []
 
     def truncate(self, seq_id: int, length: int) -> None:
         """Drop every row of a sequence beyond the first `length` (restores the

@@ -19,6 +19,7 @@ __all__ = [
     "PrefillShape",
     "attention_flops",
     "b200_profile",
+    "calibrate_b200",
     "choose_strategy",
     "comm_bytes",
     "pass_kv_overlap_min_T",
@@ -171,9 +172,12 @@ def profile(name: str, model=LLAMA3_405B, n_ranks: int = 4) -> CostModel:
 
 def b200_profile(model=LLAMA3_405B, n_ranks: int = 8, attn_efficiency: float | None = None,
                  link_gbs: float = 770.0) -> CostModel:
-    """B200 / NVLink-5 constants: C = measured bf16 peak x attention efficiency
-    (the fraction our K1 sustains; default from the latest bench in profiles/),
-    BW = measured NVLink copy per direction (B200_PROFILING.md: 770 GB/s)."""
+    """B200 / NVLink-5 constants without a measurement in this run: C =
+    measured bf16 peak x attention efficiency (default 0.74: K1's measured
+    fraction of the burst peak, profiles/r02_*), BW = measured NVLink copy per
+    direction (B200_PROFILING.md: 770 GB/s).  ``calibrate_b200`` measures all
+    of them on the box instead (what TurnRunner(calibrate=True) and
+    tools/bench_configs.py --calibrate use)."""
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     peak = 1590e12
     try:
@@ -181,10 +185,98 @@ def b200_profile(model=LLAMA3_405B, n_ranks: int = 8, attn_efficiency: float | N
             peak = float(json.load(f)["bf16_tflops"]) * 1e12
     except Exception:
         pass
-    eff = 0.65 if attn_efficiency is None else attn_efficiency
+    eff = 0.74 if attn_efficiency is None else attn_efficiency
     return CostModel(**model, n_ranks=n_ranks, peak_compute=peak * eff, bandwidth=link_gbs * 1e9,
                      sendrecv_latency_s=15e-6, a2a_base_s=30e-6)
 
 
 def with_ranks(m: CostModel, n_ranks: int) -> CostModel:
     return replace(m, n_ranks=n_ranks)
+
+
+def calibrate_b200(comm, model=LLAMA3_405B, n_ranks: int | None = None, device=None, step_tokens: int = 8192,
+                   link_bytes: int = 64 << 20, reps: int = 5):
+    """On-box calibration of the B200 cost model (SPEC.md:372-390, 422;
+    PAPER.md:556-564): measure, in THIS run, the constants Alg. 1 and the
+    refined rule need instead of assuming them.
+
+    * C: TF/s of one attention launch at a ring-step shape (``step_tokens``
+      queries x keys, causal, the model's heads) — the kernel's sustained rate;
+    * BW and SendRecv latency: one ring exchange (``comm.exchange``) of
+      ``link_bytes`` and of 4 KB, per direction;
+    * All2All: affine fit of ``comm.all_to_all`` at two sizes.
+
+    Collective over the ring (every rank calls it).  With one rank the link
+    terms keep the measured NVLink copy figure (770 GB/s).  Returns
+    (CostModel, dict of the measurements)."""
+    import statistics
+
+    import torch
+
+    from . import _lib
+    from .attention import attend_into
+
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    n = n_ranks if n_ranks is not None else getattr(comm, "world", 1)
+    hq, hkv, d = model["n_query_heads"], model["n_kv_heads"], model["head_dim"]
+
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize(dev)
+        ts = []
+        for _ in range(reps):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            torch.cuda.synchronize(dev)
+            ts.append(s.elapsed_time(e) * 1e-3)
+        return statistics.median(ts)
+
+    T = step_tokens
+    g = torch.Generator(device=dev).manual_seed(0)
+    q = torch.randn((T, hq, d), generator=g, device=dev, dtype=torch.bfloat16)
+    k = torch.randn((T, hkv, d), generator=g, device=dev, dtype=torch.bfloat16)
+    v = torch.randn((T, hkv, d), generator=g, device=dev, dtype=torch.bfloat16)
+    pos = torch.arange(T, device=dev, dtype=torch.int32)
+    seq = torch.zeros(T, device=dev, dtype=torch.int32)
+    out = torch.empty((T, hq, d), device=dev, dtype=torch.float32)
+    lse = torch.empty((T, hq), device=dev, dtype=torch.float32)
+    ws = torch.empty(_lib.load().rcp_attn_workspace_bytes(T, T), dtype=torch.uint8, device=dev)
+    t_attn = timed(lambda: attend_into(q, (pos, seq), k, v, (pos, seq), hq, hkv, d ** -0.5, out, lse,
+                                       _lib.MODE_OVERWRITE, workspace=ws))
+    flops = 4.0 * d * hq * T * (T + 1) / 2
+    meas = {"attn_tflops": flops / t_attn / 1e12, "attn_shape": f"{T}x{T} causal, {hq}/{hkv} heads"}
+    bw, lat, a2a_base, a2a_per_byte = 770e9, 15e-6, 30e-6, None
+    if n > 1:
+        big = torch.empty(link_bytes, dtype=torch.uint8, device=dev)
+        big_r = torch.empty_like(big)
+        small = torch.empty(4096, dtype=torch.uint8, device=dev)
+        small_r = torch.empty_like(small)
+        t_big = timed(lambda: comm.wait(comm.exchange(big, big_r)))
+        t_small = timed(lambda: comm.wait(comm.exchange(small, small_r)))
+        lat = t_small
+        bw = link_bytes / max(t_big - t_small, 1e-9)
+        sizes = (1 << 20, 16 << 20)
+        ts = []
+        for sz in sizes:
+            sends = [torch.empty(sz // n, dtype=torch.uint8, device=dev) for _ in range(n)]
+            recvs = [torch.empty_like(x) for x in sends]
+            ts.append(timed(lambda: comm.wait(comm.all_to_all(sends, recvs))))
+        per_rank_bytes = [(n - 1) * sz // n for sz in sizes]
+        a2a_per_byte = max((ts[1] - ts[0]) / (per_rank_bytes[1] - per_rank_bytes[0]), 0.0)
+        a2a_base = max(ts[0] - a2a_per_byte * per_rank_bytes[0], 0.0)
+        # one consistent set of constants on every rank: the slowest rank's
+        vals = torch.tensor([meas["attn_tflops"], bw, lat, a2a_base, a2a_per_byte], dtype=torch.float64, device=dev)
+        lo = vals.clone()
+        comm.dist.all_reduce(lo, op=comm.dist.ReduceOp.MIN, group=comm.group)
+        hi = vals.clone()
+        comm.dist.all_reduce(hi, op=comm.dist.ReduceOp.MAX, group=comm.group)
+        meas["attn_tflops"], bw = float(lo[0]), float(lo[1])
+        lat, a2a_base, a2a_per_byte = float(hi[2]), float(hi[3]), float(hi[4])
+    meas.update({"link_gbs": bw / 1e9, "sendrecv_latency_us": lat * 1e6, "a2a_base_us": a2a_base * 1e6,
+                 "a2a_per_byte_ns": None if a2a_per_byte is None else a2a_per_byte * 1e9})
+    m = CostModel(**model, n_ranks=n, peak_compute=meas["attn_tflops"] * 1e12, bandwidth=bw,
+                  sendrecv_latency_s=lat, a2a_base_s=a2a_base, a2a_per_byte_s=a2a_per_byte)
+    return m, meas

@@ -80,15 +80,21 @@ class TurnRunner:
     """Per-rank conversation state + turn execution over a ``RingAttention``."""
 
     def __init__(self, ring: RingAttention, cache: RankKvCache, cfg: GqaConfig, strategy: str = "adaptive",
-                 cost_model: pm.CostModel | None = None, refined: bool = False, gather_decode: bool = False):
+                 cost_model: pm.CostModel | None = None, refined: bool = False, gather_decode: bool = False,
+                 calibrate: bool = False):
+        """``calibrate=True``: the adaptive rule's constants are measured on this
+        box by ``perf_model.calibrate_b200`` (collective: every rank builds its
+        runner together) instead of the static B200 profile."""
         if strategy not in STRATEGIES:
             raise ValueError(f"strategy must be one of {STRATEGIES}, got {strategy!r}")
         self.ring, self.cache, self.cfg = ring, cache, cfg
         self.n, self.rank = ring.comm.world, ring.comm.rank
         self.strategy, self.refined, self.gather_decode = strategy, refined, gather_decode
-        self.cost_model = cost_model or pm.b200_profile(
-            dict(n_query_heads=cfg.n_query_heads, n_kv_heads=cfg.n_kv_heads, head_dim=cfg.head_dim),
-            n_ranks=self.n)
+        model = dict(n_query_heads=cfg.n_query_heads, n_kv_heads=cfg.n_kv_heads, head_dim=cfg.head_dim)
+        self.calibration = None
+        if cost_model is None and calibrate:
+            cost_model, self.calibration = pm.calibrate_b200(ring.comm, model, n_ranks=self.n, device=cache.device)
+        self.cost_model = cost_model or pm.b200_profile(model, n_ranks=self.n)
         if self.cost_model.n_ranks != self.n:
             self.cost_model = pm.with_ranks(self.cost_model, self.n)
         self.layout: dict[int, list[int]] = {}   # seq id -> cached tokens per rank

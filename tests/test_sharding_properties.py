@@ -87,3 +87,24 @@ def test_decode_plans_match_oracle(n, batch, it):
     assert max(sizes) <= plan.slots_per_rank
     for b, sid in enumerate(batch):
         assert (sid, b) in plan.assignments[plan.owner(b)]
+
+
+@settings(deadline=None, max_examples=60)
+@given(n=st.integers(1, 8), B=st.integers(1, 33), k=st.integers(1, 4), it0=st.integers(0, 50))
+def test_decode_capacity_balance_invariant(n, B, k, it0):
+    """running Alg. 4 for k·N iterations on a B-sequence batch
+    leaves max - min over ranks of the cached decode tokens <= B (the plan's
+    round-robin owner rotation), and every token is owned exactly once."""
+    from paper_2411_01783_b200.sharding import plan_decode
+
+    batch = list(range(100, 100 + B))
+    per_rank = [0] * n
+    per_seq = {s: 0 for s in batch}
+    for it in range(it0, it0 + k * n):
+        plan = plan_decode(batch, n, it)
+        for r, a in enumerate(plan.assignments):
+            per_rank[r] += len(a)
+            for sid, _b in a:
+                per_seq[sid] += 1
+    assert max(per_rank) - min(per_rank) <= B
+    assert all(v == k * n for v in per_seq.values())

@@ -86,7 +86,13 @@ def run_partial(args, rank, world):
     total = args.context
     comm = TorchRingComm() if world > 1 else _LocalComm(0, 1)
     ring = RingAttention(comm)
-    m = pm.b200_profile(dict(n_query_heads=hq, n_kv_heads=hkv, head_dim=D), n_ranks=world)
+    model = dict(n_query_heads=hq, n_kv_heads=hkv, head_dim=D)
+    m = pm.b200_profile(model, n_ranks=world)
+    calib = None
+    if args.calibrate:  # the heuristic's constants measured in this run (perf_model.calibrate_b200)
+        m, calib = pm.calibrate_b200(comm if world > 1 else _LocalComm(0, 1), model, n_ranks=world)
+        if rank == 0:
+            print(json.dumps({"calibration": calib}), flush=True)
     quantum = 2 * world * 128
     for miss in args.miss:
         T = max(quantum, int(round(miss * total / quantum)) * quantum)
@@ -220,6 +226,8 @@ def main():
     ap.add_argument("--graph", action="store_true", help="decode: replay the step from a CUDA graph")
     ap.add_argument("--no-table", action="store_true",
                     help="decode --graph: upload the step metadata each step instead of the device table")
+    ap.add_argument("--calibrate", action="store_true",
+                    help="partial: feed Alg. 1 the attention / link / All2All constants measured in this run")
     ap.add_argument("--fused", action="store_true",
                     help="partial: also time pass-Q with peer-memory partials (no All2All), checked bitwise")
     ap.add_argument("--steps", type=int, default=5)
