@@ -31,7 +31,7 @@ import torch
 from . import _lib
 from .attention import GqaConfig, merge_rows_into
 from .kv_cache import RankKvCache
-from .ring import _cuda_decode
+from .ring import _cuda_decode, merge_order_of
 from .sharding import plan_decode
 
 __all__ = ["GraphedDecode"]
@@ -55,10 +55,12 @@ class GraphedDecode:
     """
 
     def __init__(self, comm, cache: RankKvCache, cfg: GqaConfig, batch, max_steps: int = 256,
-                 first_iteration: int = 0, first_positions=None):
+                 first_iteration: int = 0, first_positions=None, merge_order: str = "arrival"):
         if cache.device.type != "cuda":
             raise RuntimeError("GraphedDecode needs the cache on a CUDA device")
         self.comm, self.cache, self.cfg = comm, cache, cfg
+        merge_order_of(0, 1, merge_order)  # validates the mode
+        self.merge_mode = merge_order
         self.batch = [int(b) for b in batch]
         self.n, self.rank = comm.world, comm.rank
         self.it = int(first_iteration)
@@ -177,7 +179,7 @@ class GraphedDecode:
                      self.ws)
         d.all_to_all_single(self.recv_o, self.part_o, group=self.comm.group)
         d.all_to_all_single(self.recv_l, self.part_l, group=self.comm.group)
-        order = [(self.rank - j) % self.n for j in range(self.n)]
+        order = merge_order_of(self.rank, self.n, self.merge_mode)
         merge_rows_into([self.recv_o[s * S:(s + 1) * S] for s in order],
                         [self.recv_l[s * S:(s + 1) * S] for s in order], self.out, self.lse)
 

@@ -14,11 +14,16 @@ compute path:
   ``ring_pass_q_prefill``, ``ring_pass_q_decode`` with the SPEC's signatures —
   the same kernels, messages read directly from the other ranks' buffers.
 
-Merge order.  pass-KV folds partials in arrival order (source ranks k, k-1, ...,
-k-N+1) inside the attention epilogue (rcp_attn_fwd mode MERGE — a running
-merge, so no N partials are ever stored).  pass-Q and decode merge the
-All2All-returned partials in that same order with the same fp32 merge code,
-so pass-KV and pass-Q are bit-identical.
+Merge order.  By default pass-KV folds partials in arrival order (source
+ranks k, k-1, ..., k-N+1) inside the attention epilogue (rcp_attn_fwd mode
+MERGE — a running merge, so no N partials are ever stored); pass-Q and decode
+merge the All2All-returned partials in that same order with the same fp32
+merge code, so pass-KV and pass-Q are bit-identical.
+``merge_order="ascending"`` (RingAttention / the simulated drivers /
+GraphedDecode) folds in ascending source rank instead — the reference's
+merge_attention contract (attention.py:325-326) — bitwise
+equal to merge_attention over the per-source partials; pass-KV then stores
+the N partials and merges once at the end.
 """
 
 from __future__ import annotations
@@ -281,6 +286,24 @@ class QLayout:
         return q, pos, seq
 
 
+MERGE_ORDERS = ("arrival", "ascending")
+
+
+def merge_order_of(rank: int, n: int, mode: str = "arrival") -> list:
+    """Source ranks in the order their partials are folded.  "arrival" (the
+    default, k, k-1, ..., k-N+1) is the order a pass-KV ring sees its KV blocks,
+    so the running merge fused into the attention epilogue needs no partials
+    stored; "ascending" (0..N-1) is the reference contract of merge_attention
+    (attention.py:325-326) — bitwise identical to
+    merge_attention over the per-source partials, at the cost of storing the
+    N partials (pass-KV) before one merge."""
+    if mode == "ascending":
+        return list(range(n))
+    if mode != "arrival":
+        raise ValueError(f"merge order must be one of {MERGE_ORDERS}, got {mode!r}")
+    return [(rank - j) % n for j in range(n)]
+
+
 def kv_message_len(plan: ShardPlan) -> int:
     """Equal-size KV message per rank: sum_i L^i (Alg. 2 line 2, sharding.py:95-103)."""
     return plan.message_token_slots()
@@ -498,7 +521,10 @@ class RingAttention:
     """SPMD ring attention for one rank.  ``attend``/``merge`` default to the
     sm_100a kernels; tests inject oracle callables to check the schedule on CPU."""
 
-    def __init__(self, comm, attend=None, merge=None, decode=None, device=None):
+    def __init__(self, comm, attend=None, merge=None, decode=None, device=None, merge_order: str = "arrival"):
+        if merge_order not in MERGE_ORDERS:
+            raise ValueError(f"merge order must be one of {MERGE_ORDERS}, got {merge_order!r}")
+        self.merge_mode = merge_order
         self.comm = comm
         self.attend = attend or _cuda_attend
         self.merge = merge or _cuda_merge
@@ -542,6 +568,9 @@ class RingAttention:
         bufs = [self._buf(("kv", 0), kv_lay.nbytes, dev), self._buf(("kv", 1), kv_lay.nbytes, dev)]
         cur = kv_msg
         pre = self._pregathered if self.no_comm == "pregathered" else None
+        parts = None
+        if self.merge_mode == "ascending" and n > 1:
+            parts = [(torch.empty_like(out), torch.empty_like(lse)) for _ in range(n)]
         for step in range(n):
             works = None
             nxt = None
@@ -556,14 +585,24 @@ class RingAttention:
                     self.trace.add(step, k, "KV", kv_lay.nbytes)
             kk, vv, kp, ks = kv_lay.views(cur, dtype)
             mode = _lib.MODE_OVERWRITE if step == 0 else _lib.MODE_MERGE
+            src = (k - step) % n
+            o_dst, l_dst = out, lse
+            if parts is not None:  # ascending merge order: keep this source's partial
+                mode = _lib.MODE_OVERWRITE
+                o_dst, l_dst = parts[src]
             for i, (a, b) in enumerate(splits):
                 if step == 0 and q_ready is not None:
                     torch.cuda.current_stream().wait_event(q_ready[i])
-                self.attend(q[a:b], q_pos[a:b], q_seq[a:b], kk, vv, kp, ks, cfg, out[a:b], lse[a:b], mode)
-                if step == n - 1 and on_final is not None:
+                self.attend(q[a:b], q_pos[a:b], q_seq[a:b], kk, vv, kp, ks, cfg, o_dst[a:b], l_dst[a:b], mode)
+                if step == n - 1 and on_final is not None and parts is None:
                     on_final(i)
             self.comm.wait(works)
             cur = nxt
+        if parts is not None:
+            self.merge([parts[s][0] for s in range(n)], [parts[s][1] for s in range(n)], out, lse)
+            if on_final is not None:
+                for i in range(len(splits)):
+                    on_final(i)
         return out, lse
 
     def pregather_kv(self) -> None:
@@ -829,7 +868,7 @@ class RingAttention:
             self.comm.stream_barrier(dev)  # every partial for this rank has landed
             if self.trace is not None:
                 self.trace.add(n - 1, k, "A2A", 0)
-            order = [(k - j) % n for j in range(n)]
+            order = merge_order_of(k, n, self.merge_mode)
             self.merge([pp.o(k, s) for s in order], [pp.lse(k, s) for s in order], out, lse)
             return out, lse
         send_o = [torch.empty((S, H, D), dtype=torch.float32, device=dev) for _ in range(n)]
@@ -857,7 +896,7 @@ class RingAttention:
             self.trace.add(n - 1, k, "A2A", (n - 1) * (send_o[0].numel() + send_l[0].numel()) * 4)
         self.comm.wait(w1)
         self.comm.wait(w2)
-        order = [(k - j) % n for j in range(n)]
+        order = merge_order_of(k, n, self.merge_mode)
         self.merge([recv_o[s] for s in order], [recv_l[s] for s in order], out, lse)
         return out, lse
 
@@ -955,7 +994,7 @@ class RingAttention:
         self.comm.wait(w2)
         out = torch.empty((slots, H, D), dtype=torch.float32, device=dev)
         lse = torch.empty((slots, H), dtype=torch.float32, device=dev)
-        order = [(k - j) % n for j in range(n)]
+        order = merge_order_of(k, n, self.merge_mode)
         self.merge([recv_o[s] for s in order], [recv_l[s] for s in order], out, lse)
         return out, lse
 
@@ -997,7 +1036,7 @@ class RingAttention:
         self.comm.wait(w)
         out = torch.empty((slots, H, D), dtype=torch.float32, device=dev)
         lse = torch.empty((slots, H), dtype=torch.float32, device=dev)
-        order = [(k - j) % n for j in range(n)]
+        order = merge_order_of(k, n, self.merge_mode)
         self.merge([ro[s] for s in order], [rl[s] for s in order], out, lse)
         return out, lse
 
@@ -1030,9 +1069,12 @@ class _LocalComm:
 
 
 def ring_pass_kv_prefill(plan: ShardPlan, caches: list, q_blocks: list, k_blocks: list,
-                         v_blocks: list, cfg: GqaConfig, trace: StepTrace | None = None):
+                         v_blocks: list, cfg: GqaConfig, trace: StepTrace | None = None,
+                         merge_order: str = "arrival"):
     """Alg. 2 over N simulated ranks on one GPU.  Returns the
-    per-rank merged PartialAttention list (and fills `trace` if given)."""
+    per-rank merged PartialAttention list (and fills `trace` if given).
+    ``merge_order="ascending"`` folds the per-source partials in ascending
+    source rank (the reference contract) with one merge at the end."""
     n = plan.n_ranks
     for r in range(n):
         append_new_tokens(plan, r, caches[r], k_blocks[r], v_blocks[r])
@@ -1044,21 +1086,30 @@ def ring_pass_kv_prefill(plan: ShardPlan, caches: list, q_blocks: list, k_blocks
         qp, qs = q.meta32("q")
         out = torch.empty((q.n_tokens, cfg.n_query_heads, cfg.head_dim), dtype=torch.float32, device=qd.device)
         lse = torch.empty((q.n_tokens, cfg.n_query_heads), dtype=torch.float32, device=qd.device)
+        parts = {}
         for step in range(n):
             src = (r - step) % n
             lay, buf = msgs[src]
             kk, vv, kp, ks = lay.views(buf, caches[src].dtype)
-            _cuda_attend(qd, qp, qs, kk, vv, kp, ks, cfg, out, lse,
-                         _lib.MODE_OVERWRITE if step == 0 else _lib.MODE_MERGE)
+            if merge_order == "ascending" and n > 1:
+                parts[src] = (torch.empty_like(out), torch.empty_like(lse))
+                _cuda_attend(qd, qp, qs, kk, vv, kp, ks, cfg, parts[src][0], parts[src][1], _lib.MODE_OVERWRITE)
+            else:
+                _cuda_attend(qd, qp, qs, kk, vv, kp, ks, cfg, out, lse,
+                             _lib.MODE_OVERWRITE if step == 0 else _lib.MODE_MERGE)
             if trace is not None and step < n - 1:
                 trace.add(step, r, "KV", lay.nbytes)
+        if parts:
+            order = merge_order_of(r, n, merge_order)
+            _cuda_merge([parts[s][0] for s in order], [parts[s][1] for s in order], out, lse)
         outs.append(PartialAttention(EmbeddingBlock(out, q.positions, q.valid, q.seq_ids, validate=False,
                                                     n_valid=q.n_valid), lse))
     return outs
 
 
 def ring_pass_q_prefill(plan: ShardPlan, caches: list, q_blocks: list, k_blocks: list,
-                        v_blocks: list, cfg: GqaConfig, trace: StepTrace | None = None):
+                        v_blocks: list, cfg: GqaConfig, trace: StepTrace | None = None,
+                        merge_order: str = "arrival"):
     """Alg. 3 over N simulated ranks: rank s computes O_r^s for
     every visiting Q_r against its resident KV; the All2All returns them and rank
     r merges in pass-KV arrival order — bit-identical to ring_pass_kv_prefill."""
@@ -1082,7 +1133,7 @@ def ring_pass_q_prefill(plan: ShardPlan, caches: list, q_blocks: list, k_blocks:
                 trace.add(step, s, "Q", QLayout(q.n_tokens, cfg.n_query_heads, cfg.head_dim).nbytes)
     outs = []
     for r in range(n):
-        order = [(r - j) % n for j in range(n)]
+        order = merge_order_of(r, n, merge_order)
         q = q_blocks[r]
         out = torch.empty_like(held[(r, r)][0])
         lse = torch.empty_like(held[(r, r)][1])
@@ -1095,7 +1146,7 @@ def ring_pass_q_prefill(plan: ShardPlan, caches: list, q_blocks: list, k_blocks:
 
 
 def ring_pass_q_decode(plan: DecodePlan, caches: list, q_tok: torch.Tensor, k_tok: torch.Tensor,
-                       v_tok: torch.Tensor, positions, cfg: GqaConfig):
+                       v_tok: torch.Tensor, positions, cfg: GqaConfig, merge_order: str = "arrival"):
     """Alg. 4 over N simulated ranks.  q_tok/k_tok/v_tok are
     [B, H, D] in batch order; positions[b] the token's global position.
     Returns (out [B, Hq, D], lse [B, Hq]) in batch order."""
@@ -1111,7 +1162,7 @@ def ring_pass_q_decode(plan: DecodePlan, caches: list, q_tok: torch.Tensor, k_to
     lse = torch.empty((B, H), dtype=torch.float32, device=dev)
     for b, sid in enumerate(plan.batch):
         owner = plan.owner(b)
-        order = [(owner - j) % n for j in range(n)]
+        order = merge_order_of(owner, n, merge_order)
         parts_o, parts_l = [], []
         for s in order:
             start, length = caches[s].segment(sid)
