@@ -244,7 +244,15 @@ def run_ours(args, cfg, rank, world, local_rank):
     torch.cuda.set_device(dev)
     T, hq, hkv = cfg["T"], cfg["hq"], cfg["hkv"]
     gcfg = rc.GqaConfig(hq, hkv, D)
-    plan = plan_full_prefill([SequenceSpec(0, 0, T)], world)
+    # a fused batch of --seqs sequences splits the T tokens into ragged
+    # sequences (lengths ~ 1 : 2 : ... : K); the default is one sequence
+    K = max(1, args.seqs)
+    w = np.arange(1, K + 1, dtype=np.float64)
+    seq_lens = np.floor(T * w / w.sum()).astype(np.int64)
+    seq_lens[-1] += T - int(seq_lens.sum())
+    seq_lens = [int(x) for x in seq_lens]
+    seq_off = np.concatenate([[0], np.cumsum(seq_lens)]).astype(np.int64)
+    plan = plan_full_prefill([SequenceSpec(i, 0, L) for i, L in enumerate(seq_lens)], world)
 
     # synthetic bf16 inputs, identical on every rank / every CP size (fixed seeds)
     gen = torch.Generator(device=dev)
@@ -257,11 +265,13 @@ def run_ours(args, cfg, rank, world, local_rank):
     ring = RingAttention(comm)
     cache = RankKvCache(hkv, D, capacity_tokens=plan.total_query_slots() + 4096, device=dev)
 
+    per_seq = {n: [t[seq_off[i]:seq_off[i + 1]] for i in range(K)] for n, t in tens.items()}
     # exact algorithmic work: admitted pairs of this rank's queries vs every source block
-    qpos = np.concatenate([plan.rank_local_indices(0, rank)])
-    qpos = qpos[qpos >= 0]
-    rank_pairs = causal_pairs(qpos, np.arange(T))
-    total_pairs = T * (T + 1) // 2
+    rank_pairs = 0
+    for i, L in enumerate(seq_lens):
+        qpos = plan.rank_local_indices(i, rank)
+        rank_pairs += causal_pairs(qpos[qpos >= 0], np.arange(L))
+    total_pairs = sum(L * (L + 1) // 2 for L in seq_lens)
     flops_rank = 4.0 * D * hq * rank_pairs
     flops_total = 4.0 * D * hq * total_pairs
 
@@ -284,9 +294,9 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     def step():
         cache.reset()
-        qb = materialize_rank_block(plan, rank, [tens["q"]])
-        kb = materialize_rank_block(plan, rank, [tens["k"]])
-        vb = materialize_rank_block(plan, rank, [tens["v"]])
+        qb = materialize_rank_block(plan, rank, per_seq["q"])
+        kb = materialize_rank_block(plan, rank, per_seq["k"])
+        vb = materialize_rank_block(plan, rank, per_seq["v"])
         return ring.pass_kv_prefill(plan, cache, qb, kb, vb, gcfg)
 
     def barrier():
@@ -330,11 +340,15 @@ def run_ours(args, cfg, rank, world, local_rank):
     # sampled query rows of the LAST timed step vs the fp64 oracle
     parity = None
     if args.check:
-        from oracle.sampled_check import check_rank_rows
+        from oracle.sampled_check import check_plan_rows, check_rank_rows
 
         rows_n = args.check_rows or {"8b": 32, "405b": 16, "405b-1m": 4}[args.config]
-        res = check_rank_rows(T, world, rank, last.output.data, last.lse, tens["q"], tens["k"], tens["v"],
-                              hkv, gcfg.scale, count=rows_n)
+        if K == 1:
+            res = check_rank_rows(T, world, rank, last.output.data, last.lse, tens["q"], tens["k"], tens["v"],
+                                  hkv, gcfg.scale, count=rows_n)
+        else:
+            res = check_plan_rows(plan, rank, last.output.data, last.lse, per_seq["q"], per_seq["k"], per_seq["v"],
+                                  hkv, gcfg.scale, rows_per_seq=max(2, rows_n // K))
         agg = torch.tensor([res["max_dO"], res["max_dLSE"], float(res["rows"])], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(agg[:2], op=dist.ReduceOp.MAX)
@@ -372,17 +386,18 @@ def run_ours(args, cfg, rank, world, local_rank):
     # ---------------- e2e through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        host = {n: t.cpu().pin_memory() for n, t in tens.items()}
+        host_full = {n: t.cpu().pin_memory() for n, t in tens.items()}
+        host = {n: [t[seq_off[i]:seq_off[i + 1]] for i in range(K)] for n, t in host_full.items()}
         s_slots = plan.total_query_slots()
         out_host = torch.empty((s_slots, hq, D), dtype=torch.float32).pin_memory()
         lse_host = torch.empty((s_slots, hq), dtype=torch.float32).pin_memory()
         h2d = 0
-        for n, t in host.items():
-            h2d += t[0].numel() * t.element_size() * (T // world)  # rank's two chunks
+        for n, t in host_full.items():  # this rank's two chunks of every sequence
+            h2d += t[0].numel() * t.element_size() * sum(plan.new_token_count(i, rank) for i in range(K))
         d2h = out_host.numel() * 4 + lse_host.numel() * 4
 
         def stage():
-            return ring.stage_host_inputs(plan, [host["q"]], [host["k"]], [host["v"]], gcfg, dev)
+            return ring.stage_host_inputs(plan, host["q"], host["k"], host["v"], gcfg, dev)
 
         def e2e_steps(n):
             # public host-buffer API as a serving loop: each request's K/V and
@@ -394,7 +409,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             st = stage()
             for i in range(n):
                 cache.reset()
-                ring.pass_kv_prefill_host(plan, cache, [host["q"]], [host["k"]], [host["v"]], gcfg, out_host,
+                ring.pass_kv_prefill_host(plan, cache, host["q"], host["k"], host["v"], gcfg, out_host,
                                           lse_host, staged=st, join=False)
                 st = stage() if i + 1 < n else None  # next request's H2D runs under this one
             ring.join_host_copies()
@@ -434,6 +449,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "data": "synthetic",
         "config": {"workload": cfg["workload"], "seq_len": T, "n_q_heads": hq, "n_kv_heads": hkv,
                    "head_dim": D, "cp": world, "protocol": "pass_kv", "parallelism": f"cp{world}",
+                   "sequences": K, **({"seq_lens": seq_lens} if K > 1 else {}),
                    "l2": "inputs larger than L2 (Q %.0f MB, K/V %.0f MB per rank)" % (
                        T // world * hq * D * 2 / 1e6, T // world * hkv * D * 2 / 1e6)},
         "latency_ms": ms, "tflops_per_gpu": value / world,
@@ -461,6 +477,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="8b", choices=sorted(CONFIGS))
     ap.add_argument("--seq-len", type=int, default=None)
+    ap.add_argument("--seqs", type=int, default=1,
+                    help="fused batch: split the tokens into this many ragged sequences (1 : 2 : ... : K)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=8)
@@ -475,6 +493,8 @@ def main():
         T = args.seq_len
         tok = f"{T >> 20}m" if T % (1 << 20) == 0 else (f"{T >> 10}k" if T % 1024 == 0 else str(T))
         cfg["workload"] = f"{model}-attn-{tok}-full-prefill-pass-kv"
+    if args.seqs > 1:
+        cfg["workload"] = cfg["workload"].replace("-full-prefill-", f"-fused{args.seqs}-varlen-prefill-")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

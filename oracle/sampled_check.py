@@ -73,3 +73,48 @@ def check_rank_rows(T: int, n_ranks: int, rank: int, out, lse, q_dev, k_dev, v_d
         d_lse = float(np.abs(got_l[fin] - want_l[fin]).max()) if fin.any() else 0.0
     return {"rows": int(toks.size), "max_dO": float(np.abs(got_o - want_o).max()), "max_dLSE": d_lse,
             "oracle_s": dt}
+
+
+def check_plan_rows(plan, rank: int, out, lse, q_seqs, k_seqs, v_seqs, n_kv_heads: int, scale: float,
+                    rows_per_seq: int = 8, seed: int = 0, block: int = 16384) -> dict:
+    """Fused multi-sequence form of ``check_rank_rows``: sequence i of the plan
+    (new tokens only, full prefill) has token-ordered inputs q_seqs[i] /
+    k_seqs[i] / v_seqs[i]; rank ``rank``'s outputs are in the plan's slot order
+    (sequences concatenated, 2·chunk_len slots each).  Sampled rows of every
+    sequence that this rank owns are compared with the fp64 oracle over that
+    sequence's keys only (attention never crosses sequences)."""
+    import torch
+
+    worst_o, worst_l, rows, off = 0.0, 0.0, 0, 0
+    for i, sh in enumerate(plan.sequences):
+        T = sh.spec.new_len
+        loc = plan.rank_local_indices(i, rank)
+        cand = orc.sample_rows(T, plan.n_ranks, rows_per_seq, seed + i)
+        slot_of = {int(t): s for s, t in enumerate(loc) if t >= 0}
+        mine = [(int(t), off + slot_of[int(t)]) for t in cand if int(t) in slot_of]
+        off += loc.size
+        if not mine:
+            continue
+        toks = np.array([t for t, _ in mine], np.int64)
+        slots = torch.tensor([s for _, s in mine], dtype=torch.long, device=out.device)
+        got_o = out.index_select(0, slots).double().cpu().numpy()
+        got_l = lse.index_select(0, slots).double().cpu().numpy()
+        qd = q_seqs[i]
+        qr = qd.index_select(0, torch.from_numpy(toks).to(qd.device)).float().cpu().numpy()
+        qb = orc.blk_from_tokens(qr, toks)
+        parts = []
+        for a in range(0, min(T, int(toks.max()) + 1), block):
+            b = min(T, a + block)
+            pos = np.arange(a, b)
+            parts.append(orc.gqa_grouped(qb, orc.blk_from_tokens(k_seqs[i][a:b].float().cpu().numpy(), pos),
+                                         orc.blk_from_tokens(v_seqs[i][a:b].float().cpu().numpy(), pos),
+                                         n_kv_heads, scale))
+        want_o, want_l = orc.merge(parts)
+        fin = np.isfinite(want_l)
+        if not np.array_equal(np.isneginf(got_l), ~fin):
+            worst_l = float("inf")
+        elif fin.any():
+            worst_l = max(worst_l, float(np.abs(got_l[fin] - want_l[fin]).max()))
+        worst_o = max(worst_o, float(np.abs(got_o - want_o).max()))
+        rows += len(mine)
+    return {"rows": rows, "max_dO": worst_o, "max_dLSE": worst_l}

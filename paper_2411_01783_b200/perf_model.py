@@ -195,7 +195,7 @@ def with_ranks(m: CostModel, n_ranks: int) -> CostModel:
 
 
 def calibrate_b200(comm, model=LLAMA3_405B, n_ranks: int | None = None, device=None, step_tokens: int = 8192,
-                   link_bytes: int = 64 << 20, reps: int = 5):
+                   link_bytes: int = 256 << 20, reps: int = 5):
     """On-box calibration of the B200 cost model (SPEC.md:372-390, 422;
     PAPER.md:556-564): measure, in THIS run, the constants Alg. 1 and the
     refined rule need instead of assuming them.
@@ -220,7 +220,10 @@ def calibrate_b200(comm, model=LLAMA3_405B, n_ranks: int | None = None, device=N
     n = n_ranks if n_ranks is not None else getattr(comm, "world", 1)
     hq, hkv, d = model["n_query_heads"], model["n_kv_heads"], model["head_dim"]
 
-    def timed(fn):
+    def timed(fn, inner=1):
+        """Seconds per call: median over ``reps`` of ``inner`` back-to-back calls
+        (transfers are issued in a row, as a ring issues them, so per-call host
+        launch cost is not counted as link time)."""
         for _ in range(2):
             fn()
         torch.cuda.synchronize(dev)
@@ -228,10 +231,11 @@ def calibrate_b200(comm, model=LLAMA3_405B, n_ranks: int | None = None, device=N
         for _ in range(reps):
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
-            fn()
+            for _ in range(inner):
+                fn()
             e.record()
             torch.cuda.synchronize(dev)
-            ts.append(s.elapsed_time(e) * 1e-3)
+            ts.append(s.elapsed_time(e) * 1e-3 / inner)
         return statistics.median(ts)
 
     T = step_tokens
@@ -254,8 +258,8 @@ def calibrate_b200(comm, model=LLAMA3_405B, n_ranks: int | None = None, device=N
         big_r = torch.empty_like(big)
         small = torch.empty(4096, dtype=torch.uint8, device=dev)
         small_r = torch.empty_like(small)
-        t_big = timed(lambda: comm.wait(comm.exchange(big, big_r)))
-        t_small = timed(lambda: comm.wait(comm.exchange(small, small_r)))
+        t_big = timed(lambda: comm.wait(comm.exchange(big, big_r)), inner=8)
+        t_small = timed(lambda: comm.wait(comm.exchange(small, small_r)), inner=8)
         lat = t_small
         bw = link_bytes / max(t_big - t_small, 1e-9)
         sizes = (1 << 20, 16 << 20)
@@ -263,7 +267,7 @@ def calibrate_b200(comm, model=LLAMA3_405B, n_ranks: int | None = None, device=N
         for sz in sizes:
             sends = [torch.empty(sz // n, dtype=torch.uint8, device=dev) for _ in range(n)]
             recvs = [torch.empty_like(x) for x in sends]
-            ts.append(timed(lambda: comm.wait(comm.all_to_all(sends, recvs))))
+            ts.append(timed(lambda: comm.wait(comm.all_to_all(sends, recvs)), inner=4))
         per_rank_bytes = [(n - 1) * sz // n for sz in sizes]
         a2a_per_byte = max((ts[1] - ts[0]) / (per_rank_bytes[1] - per_rank_bytes[0]), 0.0)
         a2a_base = max(ts[0] - a2a_per_byte * per_rank_bytes[0], 0.0)

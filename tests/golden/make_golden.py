@@ -210,6 +210,7 @@ def shard_cases():
         d["message_token_slots"] = plan.message_token_slots()
         d["local_indices"] = [[plan.rank_local_indices(i, r).tolist() for r in range(n)]
                               for i in range(len(ss))]
+        d["to_json"] = plan.to_json()  # the plan wire format (--dump-plan), byte for byte
         cases.append(d)
         if max(s[2] for s in seqs) <= 128:
             data = [rng.standard_normal((s[2], 2, 4)).astype(np.float32) for s in seqs]

@@ -143,3 +143,21 @@ def test_message_layouts_and_topology():
     t = RingTopology(4)
     assert [t.next(k) for k in range(4)] == [1, 2, 3, 0]
     assert [t.source_at(1, s) for s in range(4)] == [1, 0, 3, 2]
+
+
+def test_shard_plan_json_wire_format_matches_reference_bytes():
+    """ShardPlan.to_json (sharding.py:117-141, the --dump-plan wire format,
+    SPEC.md:158/497) is byte-identical to the reference's for every golden
+    plan, and round-trips through json."""
+    import json
+
+    from paper_2411_01783_b200.sharding import SequenceSpec, plan_full_prefill, plan_partial_prefill
+
+    for c in G.js("shard.json"):
+        seqs = [SequenceSpec(s["seq_id"], s["cached_len"], s["new_len"]) for s in c["sequences"]]
+        n = c["n_ranks"]
+        plan = (plan_full_prefill(seqs, n) if c["kind"] == "full" else
+                plan_partial_prefill(seqs, n, [s["rank_cached_counts"] for s in c["sequences"]]))
+        assert plan.to_json() == c["to_json"]
+        d = json.loads(plan.to_json())
+        assert d["assignment"] == [[r, 2 * n - 1 - r] for r in range(n)]
