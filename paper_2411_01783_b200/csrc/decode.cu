@@ -343,6 +343,8 @@ __global__ void __launch_bounds__(kCombineWarps * 32) decode_combine_kernel(
 // CTA-count target of the split heuristic.  148 x 8 (about 2.7 waves of the
 // three CTAs per SM the 2-stage ring allows) measured best: 148 x 6 and
 // 148 x 3 gave 0.79 / 0.87 ms per graphed B=4 step against 0.755 ms.
+// (Round 2: 148 x 9, three full waves of 3 CTAs per SM instead of 2.65, measured
+// neutral at B = 1 (0.247 vs 0.245 ms per graphed step) and 2 % slower at B = 4.)
 #ifndef RCP_DEC_CTA_TARGET
 #define RCP_DEC_CTA_TARGET (148 * 8)
 #endif

@@ -159,13 +159,13 @@ def run_decode(args, rank, world):
     ring = RingAttention(comm)
     local = args.context // world
     for B in args.batch:
-        cache = RankKvCache(hkv, D, capacity_tokens=B * (local + 64))
+        cache = RankKvCache(hkv, D, capacity_tokens=B * (local + 128))
         batch = list(range(B))
         hplan = plan_full_prefill([SequenceSpec(0, 0, args.context)], world)
         loc = hplan.rank_local_indices(0, rank)
         pos = loc[loc >= 0]
         for b in batch:  # each sequence: its balanced shard of the history (random data)
-            cache._reserve(b, local + 64)  # room for the decode steps: no segment moves later
+            cache._reserve(b, local + 128)  # room for the decode steps: no segment moves later
             cache.append_rows(b, randn((local, hkv, D), 100 + b), randn((local, hkv, D), 200 + b), pos)
         lens = {b: cache.cached_len(b) for b in batch}
         dp = plan_decode(batch, world, 0)
@@ -191,7 +191,7 @@ def run_decode(args, rank, world):
             pos0 = {b: max(lens[b], args.context) for b in batch}
             # consecutive positions per step: the step metadata is precomputed on the
             # device and selected by the graph (no per-step upload / host metadata)
-            gd = GraphedDecode(comm, cache, cfg, batch, max_steps=args.warmup + args.steps + 2,
+            gd = GraphedDecode(comm, cache, cfg, batch, max_steps=args.warmup + 2 * args.steps + 4,
                                first_positions=None if args.no_table else pos0)
 
             def step():  # noqa: F811 - graphed variant
@@ -202,13 +202,26 @@ def run_decode(args, rank, world):
 
             reset = lambda: None  # noqa: E731 - appends are part of the measured step
         ms = timed(step, reset, args.steps, args.warmup, world)
+        b2b = None
+        if args.graph:
+            # back to back: the host issues step i+1 while the GPU runs step i
+            # (a serving loop); per-step time = max(host issue, GPU time)
+            barrier(world)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            nb = max(1, min(args.steps, gd.steps_left - 1))
+            for _ in range(nb):
+                step()
+            e.record()
+            torch.cuda.synchronize()
+            b2b = max_over_ranks(s.elapsed_time(e) / nb, world)
         kv_bytes = B * local * hkv * D * 2 * 2  # this rank's K+V read per decode step
         if rank == 0:
             print(json.dumps({
                 "config": "cfg5-ring-pass-q-decode", "cp": world, "batch": B, "context": args.context,
                 "q_transport": "allgather" if (args.gather or args.graph) else "ring",
                 "cuda_graph": bool(args.graph), "device_step_table": bool(args.graph and not args.no_table),
-                "n_q_heads": hq, "n_kv_heads": hkv, "step_ms": ms,
+                "n_q_heads": hq, "n_kv_heads": hkv, "step_ms": ms, "step_ms_back_to_back": b2b,
                 "kv_bytes_per_rank": kv_bytes, "hbm_gbs_effective": kv_bytes / (ms * 1e-3) / 1e9}), flush=True)
         del cache
         torch.cuda.empty_cache()
