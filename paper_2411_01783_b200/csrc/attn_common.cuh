@@ -157,13 +157,13 @@ __device__ __forceinline__ float2 ex2_poly_x2(float a, float b) {
 // Key-block rows of a version's tile summaries:
 inline int attn_key_rows(int version) { return version == 4 ? 64 : 128; }
 // TMA box rows of the K / V maps (v13 loads half blocks: 64 keys of K, 128 keys x 64 dims of V)
-inline int attn_k_box_rows(int version) { return version == 13 ? 64 : attn_key_rows(version); }
+inline int attn_k_box_rows(int version) { return (version == 13 || version == 14) ? 64 : attn_key_rows(version); }
 inline int attn_v_box_rows(int version) { return attn_key_rows(version); }
 #ifndef RCP_DEFAULT_ATTN_VERSION
 #define RCP_DEFAULT_ATTN_VERSION 4
 #endif
 constexpr int kDefaultAttnVersion = RCP_DEFAULT_ATTN_VERSION;
 int attn_n128_launch(const AttnParams& prm, int64_t grid, cudaStream_t st);
-int attn_pair_launch(const AttnParams& prm, int64_t n_pairs_heads, cudaStream_t st);
+int attn_pair_launch(const AttnParams& prm, int64_t n_pairs_heads, cudaStream_t st, bool col_split);
 
 }  // namespace rcp

@@ -127,6 +127,11 @@ __device__ __forceinline__ float2 unpack_bf16x2(uint32_t v) {
   return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xFFFF0000u));
 }
 
+// kColSplit = false (v13): the two softmax groups take alternate key blocks.
+// kColSplit = true (v14): both groups take every block, group g the score
+// columns [64 g, 64 g + 64) of all 128 rows (two warps per SMSP in the same
+// phase, as v4's two tiles, but on N = 128 MMAs with three S buffers).
+template <bool kColSplit>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_fwd_pair_kernel(const __grid_constant__ AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -140,6 +145,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_slot;
   __shared__ float m_xch[2][128];  // [producing group][row]: m(it) handed to the other group
   __shared__ float l_xch[2][128];  // epilogue: each group's row sum
+  __shared__ float mx2[2][2][128];  // v14: [block parity][group][row] half-block max
 
   const int warp = static_cast<int>(warp_id());
   // Pair order as v4: KV-head major, heavy (late) query blocks first, then the
@@ -165,7 +171,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < kSBufP; ++b) {
       mbar_init(&bar_s[b], 1);
-      mbar_init(&bar_p[b], 2 * 4);  // the four warps of the block's softmax group, in both CTAs
+      // v13: the four warps of the block's softmax group; v14: all eight; in both CTAs
+      mbar_init(&bar_p[b], kColSplit ? 2 * 8 : 2 * 4);
     }
     mbar_init(&bar_pv[0], 1);  // PV(it) completions, it even / odd
     mbar_init(&bar_pv[1], 1);
@@ -249,9 +256,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         auto issue_pv = [&](int buf, uint32_t ld, bool acc) {
           const uint32_t va = v_lo + (((ld % kSlotsP) * kSlotBytesP) >> 4);
 #pragma unroll
-          for (int kk = 0; kk < kKRowsP / 16; ++kk)
-            mma2_ts(tmem + kTmemOP, tmem + kTmemSP + buf * 128 + kk * 8, va + ((kk * 2048) >> 4), idesc_o,
+          for (int kk = 0; kk < kKRowsP / 16; ++kk) {
+            // P columns of keys [16 kk, 16 kk + 16): v13 packs all 128 keys over the first 64
+            // columns of the S buffer; v14's groups each pack theirs over the first 32 of
+            // their own 64 S columns
+            const uint32_t pcol = kColSplit ? (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8) : kk * 8;
+            mma2_ts(tmem + kTmemOP, tmem + kTmemSP + buf * 128 + pcol, va + ((kk * 2048) >> 4), idesc_o,
                     (acc || kk > 0) ? 1u : 0u);
+          }
         };
         mbar_wait(&bar_q, 0);
         for (int b = 0; b < kSBufP && b < n; ++b) {
@@ -312,39 +324,208 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     float m = -INFINITY;   // m (log2 units) after the last block this group processed
     float mg = -INFINITY;  // the m this group's row sum lg is expressed in
     float lg = 0.f;
-    int it = g;
-    for (; it < n; it += 2) {
-      const int buf = it % kSBufP;
-      const uint32_t s_addr = lane_base + kTmemSP + buf * 128;
-      const uint32_t e = __ldg(act + it);
-      const int j = act_j(e);
-      const int cls = act_cls(e, rank);
-      // mask bits of a PARTIAL block (bit c: key c admitted), before S is live
-      uint32_t mbits[4] = {~0u, ~0u, ~0u, ~0u};
-      if (cls == kTilePartial) {
-        const int base = j * kKRowsP;
-        if (base + kKRowsP <= p.tk) {
-          const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + base);
-          const int4* ks4 = reinterpret_cast<const int4*>(p.k_seq + base);
-#pragma unroll 1
-          for (int gq = 0; gq < 4; ++gq) {  // (not unrolled: 8 int4 pairs in flight, not 64)
-            uint32_t bits = 0;
-#pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4) {
-              const int4 kp = __ldg(kp4 + 8 * gq + c4), kq = __ldg(ks4 + 8 * gq + c4);
-              bits |= static_cast<uint32_t>(kq.x == my_seq && kp.x <= my_pos) << (4 * c4 + 0);
-              bits |= static_cast<uint32_t>(kq.y == my_seq && kp.y <= my_pos) << (4 * c4 + 1);
-              bits |= static_cast<uint32_t>(kq.z == my_seq && kp.z <= my_pos) << (4 * c4 + 2);
-              bits |= static_cast<uint32_t>(kq.w == my_seq && kp.w <= my_pos) << (4 * c4 + 3);
+    if constexpr (!kColSplit) {
+      int it = g;
+      for (; it < n; it += 2) {
+        const int buf = it % kSBufP;
+        const uint32_t s_addr = lane_base + kTmemSP + buf * 128;
+        const uint32_t e = __ldg(act + it);
+        const int j = act_j(e);
+        const int cls = act_cls(e, rank);
+        // mask bits of a PARTIAL block (bit c: key c admitted), before S is live
+        uint32_t mbits[4] = {~0u, ~0u, ~0u, ~0u};
+        if (cls == kTilePartial) {
+          const int base = j * kKRowsP;
+          if (base + kKRowsP <= p.tk) {
+            const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + base);
+            const int4* ks4 = reinterpret_cast<const int4*>(p.k_seq + base);
+  #pragma unroll 1
+            for (int gq = 0; gq < 4; ++gq) {  // (not unrolled: 8 int4 pairs in flight, not 64)
+              uint32_t bits = 0;
+  #pragma unroll
+              for (int c4 = 0; c4 < 8; ++c4) {
+                const int4 kp = __ldg(kp4 + 8 * gq + c4), kq = __ldg(ks4 + 8 * gq + c4);
+                bits |= static_cast<uint32_t>(kq.x == my_seq && kp.x <= my_pos) << (4 * c4 + 0);
+                bits |= static_cast<uint32_t>(kq.y == my_seq && kp.y <= my_pos) << (4 * c4 + 1);
+                bits |= static_cast<uint32_t>(kq.z == my_seq && kp.z <= my_pos) << (4 * c4 + 2);
+                bits |= static_cast<uint32_t>(kq.w == my_seq && kp.w <= my_pos) << (4 * c4 + 3);
+              }
+  #pragma unroll
+              for (int x = 0; x < 4; ++x) mbits[x] = gq == x ? bits : mbits[x];
             }
-#pragma unroll
-            for (int x = 0; x < 4; ++x) mbits[x] = gq == x ? bits : mbits[x];
+          } else {
+  #pragma unroll
+            for (int gq = 0; gq < 4; ++gq) {  // (unrolled: mbits stays in registers)
+              uint32_t bits = 0;
+  #pragma unroll 1
+              for (int c = 0; c < 32; ++c) {
+                const int kidx = base + 32 * gq + c;
+                const bool ok = kidx < p.tk && __ldg(p.k_seq + kidx) == my_seq && __ldg(p.k_pos + kidx) <= my_pos;
+                bits |= static_cast<uint32_t>(ok) << c;
+              }
+              mbits[gq] = bits;
+            }
           }
+        }
+        mbar_wait(&bar_s[buf], (it / kSBufP) & 1);
+        tc_fence_after();
+        if (t == 0) TRACE(2 + 2 * g, it >> 1);
+        // The running max m(it) = lazy(m(it-1), max of block it) chains the
+        // blocks of both groups: group g takes m(it-1) from the other group and
+        // hands m(it) on.  The exps run first, with the provisional m of the
+        // group's own chain, so they never wait; the exact m(it) is settled after
+        // them, and in the rare case it differs (the other group raised m at
+        // it-1) this row's P and block sum are rescaled by the exact power of two.
+        uint32_t s[128];  // scores (fp32 bits) of this row
+        float mx = -INFINITY;
+        if (cls != kTileEmpty) {  // uniform across the CTA
+          tmem_ld64(s_addr, s);
+          tmem_ld64(s_addr + 64, s + 64);
+          tmem_ld_wait();
+          if (cls == kTilePartial) {
+  #pragma unroll
+            for (int c = 0; c < 128; ++c)
+              if (!((mbits[c >> 5] >> (c & 31)) & 1u)) s[c] = 0xFF800000u;  // -inf
+          }
+          float m8[8];
+  #pragma unroll
+          for (int k = 0; k < 8; ++k)
+            m8[k] = fmax3(__uint_as_float(s[k]), __uint_as_float(s[8 + k]), __uint_as_float(s[16 + k]));
+  #pragma unroll
+          for (int c = 24; c < 120; c += 16)
+  #pragma unroll
+            for (int k = 0; k < 8; ++k) m8[k] = fmax3(m8[k], __uint_as_float(s[c + k]), __uint_as_float(s[c + 8 + k]));
+  #pragma unroll
+          for (int k = 0; k < 8; ++k) m8[k] = fmaxf(m8[k], __uint_as_float(s[120 + k]));
+          mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+        }
+        if (t == 0 && g == 0) TRACE(8, it >> 1);
+        const float mx_l2 = mx * sl2;
+        // provisional m of this block from this group's own chain (m holds m(it-2)):
+        // the exps never wait for the other group
+        const float m_prov = lazy_max(m, mx_l2);  // m: this group's m after its previous block
+        float bsum = 0.f;
+        if (cls != kTileEmpty) {
+          const float m_use = (m_prov == -INFINITY) ? 0.f : m_prov;
+          const uint64_t negm2 = f2(-m_use, -m_use);
+          uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+          auto exp_chunks = [&](auto full) {
+  #pragma unroll
+            for (int q = 0; q < 4; ++q) {  // 32 keys -> 16 packed P columns per chunk
+              uint32_t pk[16];
+  #pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const int ip = 16 * q + i;
+                const float2 x =
+                    unf2(ffma2(f2(__uint_as_float(s[2 * ip]), __uint_as_float(s[2 * ip + 1])), sl2x2, negm2));
+                float p0, p1;
+                if (decltype(full)::value && (ip & 7) < kPolyPairsP) {
+                  const float2 pp = ex2_poly_x2(x.x, x.y);
+                  p0 = pp.x;
+                  p1 = pp.y;
+                } else {
+                  p0 = ex2_approx(x.x);
+                  p1 = ex2_approx(x.y);
+                }
+                acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
+                pk[i] = pack_bf16x2(p0, p1);
+              }
+              tmem_st16(s_addr + 16 * q, pk);
+            }
+          };
+          if (cls == kTileFull) {
+            exp_chunks(std::true_type{});
+          } else {
+            exp_chunks(std::false_type{});
+          }
+          const float2 a01 = unf2(fadd2(acc2[0], acc2[1]));
+          const float2 a23 = unf2(fadd2(acc2[2], acc2[3]));
+          bsum = (a01.x + a01.y) + (a23.x + a23.y);
         } else {
+          uint32_t pk[32];
+  #pragma unroll
+          for (int i = 0; i < 32; ++i) pk[i] = 0u;
+          tmem_st32(s_addr, pk);
+          tmem_st32(s_addr + 32, pk);
+        }
+        if (t == 0 && g == 0) TRACE(9, it >> 1);
+        // settle m(it): take m(it-1) from the other group, hand m(it) on
+        const float m_in = it > 0 ? (named_bar_sync(bar_take, 64), m_xch[g ^ 1][t]) : -INFINITY;
+        const float m_fin = lazy_max(m_in, mx_l2);
+        if (it + 1 < n) {
+          m_xch[g][t] = m_fin;
+          named_bar_arrive(bar_give, 64);
+        }
+        if (t == 0 && g == 0) TRACE(10, it >> 1);
+        // rare: P was made with a different m (the other group raised m at it-1)
+        // -> rescale this row's P and block sum by the exact power of two
+        const bool fix_p = m_prov != m_fin && m_prov != -INFINITY && cls != kTileEmpty;
+        if (__any_sync(0xffffffffu, fix_p)) {
+          const float fp = fix_p ? ex2_approx(m_prov - m_fin) : 1.0f;
+          tmem_st_wait();
+  #pragma unroll 1
+          for (int c = 0; c < 64; c += 8) {
+            uint32_t pk[8];
+            tmem_ld8(s_addr + c, pk);
+            tmem_ld_wait();
+  #pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float2 v2 = unpack_bf16x2(pk[i]);
+              pk[i] = pack_bf16x2(v2.x * fp, v2.y * fp);
+            }
+            tmem_st8(s_addr + c, pk);
+          }
+          bsum *= fp;
+        }
+        // O rescale when block it raised m over a non-empty O: after PV(it-1)
+        // completed (PV(it) waits for this group's P)
+        const bool raised = m_fin != m_in && m_in != -INFINITY;
+        if (__any_sync(0xffffffffu, raised)) {
+          const float f = raised ? ex2_approx(m_in - m_fin) : 1.0f;
+          // PV(it-1) is phase (it-1)/2 of bar_pv[(it-1)&1]; PV(it-3) (same barrier,
+          // one phase earlier) completed before S(it) was issued and PV(it+1)
+          // cannot start before this group's P(it), so the parity is unambiguous
+          mbar_wait(&bar_pv[(it - 1) & 1], ((it - 1) >> 1) & 1);
+          tc_fence_after();
+  #pragma unroll 1
+          for (int c = 0; c < kD; c += 8) {
+            uint32_t r[8];
+            tmem_ld8(o_addr + c, r);
+            tmem_ld_wait();
+  #pragma unroll
+            for (int i = 0; i < 8; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
+            tmem_st8(o_addr + c, r);
+          }
+        }
+        m = m_fin;
+        // this group's row sum, in units of the current m
+        if (m != mg) {
+          lg = (mg == -INFINITY) ? 0.f : lg * ex2_approx(mg - m);
+          mg = m;
+        }
+        lg += bsum;
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) arrive_on_leader(&bar_p[buf]);
+        if (t == 0) TRACE(3 + 2 * g, it >> 1);
+      }
+    } else {
+      // ---- v14: every block, this group's 64 score columns
+      const uint32_t bar_x = 1 + q4;  // symmetric exchange of the half-block max (this quarter's 2 warps)
+      for (int it = 0; it < n; ++it) {
+        const int buf = it % kSBufP;
+        const uint32_t s_addr = lane_base + kTmemSP + buf * 128 + 64 * g;
+        const uint32_t e = __ldg(act + it);
+        const int j = act_j(e);
+        const int cls = act_cls(e, rank);
+        uint32_t mbits[2] = {~0u, ~0u};
+        if (cls == kTilePartial) {
+          const int base = j * kKRowsP + 64 * g;
 #pragma unroll
-          for (int gq = 0; gq < 4; ++gq) {  // (unrolled: mbits stays in registers)
+          for (int gq = 0; gq < 2; ++gq) {
             uint32_t bits = 0;
-#pragma unroll 1
+#pragma unroll 4
             for (int c = 0; c < 32; ++c) {
               const int kidx = base + 32 * gq + c;
               const bool ok = kidx < p.tk && __ldg(p.k_seq + kidx) == my_seq && __ldg(p.k_pos + kidx) <= my_pos;
@@ -353,149 +534,130 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbits[gq] = bits;
           }
         }
-      }
-      mbar_wait(&bar_s[buf], (it / kSBufP) & 1);
-      tc_fence_after();
-      if (t == 0) TRACE(2 + 2 * g, it >> 1);
-      // The running max m(it) = lazy(m(it-1), max of block it) chains the
-      // blocks of both groups: group g takes m(it-1) from the other group and
-      // hands m(it) on.  The exps run first, with the provisional m of the
-      // group's own chain, so they never wait; the exact m(it) is settled after
-      // them, and in the rare case it differs (the other group raised m at
-      // it-1) this row's P and block sum are rescaled by the exact power of two.
-      uint32_t s[128];  // scores (fp32 bits) of this row
-      float mx = -INFINITY;
-      if (cls != kTileEmpty) {  // uniform across the CTA
-        tmem_ld64(s_addr, s);
-        tmem_ld64(s_addr + 64, s + 64);
-        tmem_ld_wait();
-        if (cls == kTilePartial) {
-#pragma unroll
-          for (int c = 0; c < 128; ++c)
-            if (!((mbits[c >> 5] >> (c & 31)) & 1u)) s[c] = 0xFF800000u;  // -inf
-        }
-        float m8[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          m8[k] = fmax3(__uint_as_float(s[k]), __uint_as_float(s[8 + k]), __uint_as_float(s[16 + k]));
-#pragma unroll
-        for (int c = 24; c < 120; c += 16)
-#pragma unroll
-          for (int k = 0; k < 8; ++k) m8[k] = fmax3(m8[k], __uint_as_float(s[c + k]), __uint_as_float(s[c + 8 + k]));
-#pragma unroll
-        for (int k = 0; k < 8; ++k) m8[k] = fmaxf(m8[k], __uint_as_float(s[120 + k]));
-        mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
-      }
-      if (t == 0 && g == 0) TRACE(8, it >> 1);
-      const float mx_l2 = mx * sl2;
-      // provisional m of this block from this group's own chain (m holds m(it-2)):
-      // the exps never wait for the other group
-      const float m_prov = lazy_max(m, mx_l2);  // m: this group's m after its previous block
-      float bsum = 0.f;
-      if (cls != kTileEmpty) {
-        const float m_use = (m_prov == -INFINITY) ? 0.f : m_prov;
-        const uint64_t negm2 = f2(-m_use, -m_use);
-        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
-        auto exp_chunks = [&](auto full) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {  // 32 keys -> 16 packed P columns per chunk
-            uint32_t pk[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int ip = 16 * q + i;
-              const float2 x =
-                  unf2(ffma2(f2(__uint_as_float(s[2 * ip]), __uint_as_float(s[2 * ip + 1])), sl2x2, negm2));
-              float p0, p1;
-              if (decltype(full)::value && (ip & 7) < kPolyPairsP) {
-                const float2 pp = ex2_poly_x2(x.x, x.y);
-                p0 = pp.x;
-                p1 = pp.y;
-              } else {
-                p0 = ex2_approx(x.x);
-                p1 = ex2_approx(x.y);
-              }
-              acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
-              pk[i] = pack_bf16x2(p0, p1);
-            }
-            tmem_st16(s_addr + 16 * q, pk);
-          }
-        };
-        if (cls == kTileFull) {
-          exp_chunks(std::true_type{});
-        } else {
-          exp_chunks(std::false_type{});
-        }
-        const float2 a01 = unf2(fadd2(acc2[0], acc2[1]));
-        const float2 a23 = unf2(fadd2(acc2[2], acc2[3]));
-        bsum = (a01.x + a01.y) + (a23.x + a23.y);
-      } else {
-        uint32_t pk[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) pk[i] = 0u;
-        tmem_st32(s_addr, pk);
-        tmem_st32(s_addr + 32, pk);
-      }
-      if (t == 0 && g == 0) TRACE(9, it >> 1);
-      // settle m(it): take m(it-1) from the other group, hand m(it) on
-      const float m_in = it > 0 ? (named_bar_sync(bar_take, 64), m_xch[g ^ 1][t]) : -INFINITY;
-      const float m_fin = lazy_max(m_in, mx_l2);
-      if (it + 1 < n) {
-        m_xch[g][t] = m_fin;
-        named_bar_arrive(bar_give, 64);
-      }
-      if (t == 0 && g == 0) TRACE(10, it >> 1);
-      // rare: P was made with a different m (the other group raised m at it-1)
-      // -> rescale this row's P and block sum by the exact power of two
-      const bool fix_p = m_prov != m_fin && m_prov != -INFINITY && cls != kTileEmpty;
-      if (__any_sync(0xffffffffu, fix_p)) {
-        const float fp = fix_p ? ex2_approx(m_prov - m_fin) : 1.0f;
-        tmem_st_wait();
-#pragma unroll 1
-        for (int c = 0; c < 64; c += 8) {
-          uint32_t pk[8];
-          tmem_ld8(s_addr + c, pk);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float2 v2 = unpack_bf16x2(pk[i]);
-            pk[i] = pack_bf16x2(v2.x * fp, v2.y * fp);
-          }
-          tmem_st8(s_addr + c, pk);
-        }
-        bsum *= fp;
-      }
-      // O rescale when block it raised m over a non-empty O: after PV(it-1)
-      // completed (PV(it) waits for this group's P)
-      const bool raised = m_fin != m_in && m_in != -INFINITY;
-      if (__any_sync(0xffffffffu, raised)) {
-        const float f = raised ? ex2_approx(m_in - m_fin) : 1.0f;
-        // PV(it-1) is phase (it-1)/2 of bar_pv[(it-1)&1]; PV(it-3) (same barrier,
-        // one phase earlier) completed before S(it) was issued and PV(it+1)
-        // cannot start before this group's P(it), so the parity is unambiguous
-        mbar_wait(&bar_pv[(it - 1) & 1], ((it - 1) >> 1) & 1);
+        mbar_wait(&bar_s[buf], (it / kSBufP) & 1);
         tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < kD; c += 8) {
-          uint32_t r[8];
-          tmem_ld8(o_addr + c, r);
+        if (t == 0) TRACE(2 + 2 * g, it);
+        uint32_t s[64];
+        float mx = -INFINITY;
+        if (cls != kTileEmpty) {
+          tmem_ld64(s_addr, s);
           tmem_ld_wait();
+          if (cls == kTilePartial) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
-          tmem_st8(o_addr + c, r);
+            for (int c = 0; c < 64; ++c)
+              if (!((mbits[c >> 5] >> (c & 31)) & 1u)) s[c] = 0xFF800000u;
+          }
+          float m8[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            m8[k] = fmax3(__uint_as_float(s[k]), __uint_as_float(s[8 + k]), __uint_as_float(s[16 + k]));
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m8[k] = fmax3(m8[k], __uint_as_float(s[24 + k]), __uint_as_float(s[32 + k]));
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m8[k] = fmax3(m8[k], __uint_as_float(s[40 + k]), __uint_as_float(s[48 + k]));
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m8[k] = fmaxf(m8[k], __uint_as_float(s[56 + k]));
+          mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
         }
+        const float mx_l2 = mx * sl2;
+        // exps with the provisional m from this half's max; the exact m (both
+        // halves) is settled after them and differs only when just one half
+        // raises the lazy max (rare): then this half's P and sum are rescaled
+        const float m_prov = lazy_max(m, mx_l2);
+        float bsum = 0.f;
+        if (cls != kTileEmpty) {
+          const float m_use = (m_prov == -INFINITY) ? 0.f : m_prov;
+          const uint64_t negm2 = f2(-m_use, -m_use);
+          uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+          auto exp_chunks = [&](auto full) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              uint32_t pk[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const int ip = 16 * q + i;
+                const float2 x =
+                    unf2(ffma2(f2(__uint_as_float(s[2 * ip]), __uint_as_float(s[2 * ip + 1])), sl2x2, negm2));
+                float p0, p1;
+                if (decltype(full)::value && (ip & 7) < kPolyPairsP) {
+                  const float2 pp = ex2_poly_x2(x.x, x.y);
+                  p0 = pp.x;
+                  p1 = pp.y;
+                } else {
+                  p0 = ex2_approx(x.x);
+                  p1 = ex2_approx(x.y);
+                }
+                acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
+                pk[i] = pack_bf16x2(p0, p1);
+              }
+              tmem_st16(s_addr + 16 * q, pk);
+            }
+          };
+          if (cls == kTileFull) {
+            exp_chunks(std::true_type{});
+          } else {
+            exp_chunks(std::false_type{});
+          }
+          const float2 a01 = unf2(fadd2(acc2[0], acc2[1]));
+          const float2 a23 = unf2(fadd2(acc2[2], acc2[3]));
+          bsum = (a01.x + a01.y) + (a23.x + a23.y);
+        } else {
+          uint32_t pk[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) pk[i] = 0u;
+          tmem_st32(s_addr, pk);
+        }
+        if (t == 0 && g == 0) TRACE(9, it);
+        mx2[it & 1][g][t] = mx_l2;
+        named_bar_sync(bar_x, 64);
+        const float m_fin = lazy_max(m, fmaxf(mx_l2, mx2[it & 1][g ^ 1][t]));
+        const bool fix_p = m_prov != m_fin && m_prov != -INFINITY && cls != kTileEmpty;
+        if (__any_sync(0xffffffffu, fix_p)) {
+          const float fp = fix_p ? ex2_approx(m_prov - m_fin) : 1.0f;
+          tmem_st_wait();
+#pragma unroll 1
+          for (int c = 0; c < 32; c += 8) {
+            uint32_t pk[8];
+            tmem_ld8(s_addr + c, pk);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float2 v2 = unpack_bf16x2(pk[i]);
+              pk[i] = pack_bf16x2(v2.x * fp, v2.y * fp);
+            }
+            tmem_st8(s_addr + c, pk);
+          }
+          bsum *= fp;
+        }
+        // O rescale when block it raised m over a non-empty O: this group's 64
+        // O columns, after PV(it-1) completed
+        const bool raised = m_fin != m && m != -INFINITY;
+        if (__any_sync(0xffffffffu, raised)) {
+          const float f = raised ? ex2_approx(m - m_fin) : 1.0f;
+          mbar_wait(&bar_pv[(it - 1) & 1], ((it - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < 64; c += 8) {
+            uint32_t r[8];
+            tmem_ld8(o_addr + 64 * g + c, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
+            tmem_st8(o_addr + 64 * g + c, r);
+          }
+        }
+        m = m_fin;
+        if (m != mg) {
+          lg = (mg == -INFINITY) ? 0.f : lg * ex2_approx(mg - m);
+          mg = m;
+        }
+        lg += bsum;
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) arrive_on_leader(&bar_p[buf]);
+        if (t == 0) TRACE(3 + 2 * g, it);
       }
-      m = m_fin;
-      // this group's row sum, in units of the current m
-      if (m != mg) {
-        lg = (mg == -INFINITY) ? 0.f : lg * ex2_approx(mg - m);
-        mg = m;
-      }
-      lg += bsum;
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) arrive_on_leader(&bar_p[buf]);
-      if (t == 0) TRACE(3 + 2 * g, it >> 1);
     }
 
     // epilogue: combine the groups' sums in the final m, O / l, LSE, optional merge
@@ -562,14 +724,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
-int attn_pair_launch(const AttnParams& prm, int64_t n_pairs_heads, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    RCP_CUDA(cudaFuncSetAttribute(attn_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemBytesP));
-    attr_set = true;
+int attn_pair_launch(const AttnParams& prm, int64_t n_pairs_heads, cudaStream_t st, bool col_split) {
+  static bool attr_set[2] = {false, false};
+  auto kern = col_split ? attn_fwd_pair_kernel<true> : attn_fwd_pair_kernel<false>;
+  if (!attr_set[col_split]) {
+    RCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytesP));
+    attr_set[col_split] = true;
   }
-  attn_fwd_pair_kernel<<<static_cast<unsigned>(2 * n_pairs_heads), kThreads, kSmemBytesP, st>>>(prm);
+  kern<<<static_cast<unsigned>(2 * n_pairs_heads), kThreads, kSmemBytesP, st>>>(prm);
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
 }

@@ -195,6 +195,8 @@ class HostStage:
     kv_ready: torch.cuda.Event
     q_ready: list
     slot: int
+    idx: np.ndarray | None = None      # concatenated source row of every query slot (-1 pad)
+    seq_off: np.ndarray | None = None  # first concatenated row of every sequence
 
 
 def _slot_runs(seg: np.ndarray, seq_off: np.ndarray):
@@ -725,7 +727,7 @@ class RingAttention:
                 ev = torch.cuda.Event(enable_timing=True)
                 ev.record(s_in)
                 q_ready.append(ev)
-        return HostStage(plan, kd, vd, q, qp, qs, splits, kv_ready, q_ready, slot)
+        return HostStage(plan, kd, vd, q, qp, qs, splits, kv_ready, q_ready, slot, idx, seq_off)
 
     def join_host_copies(self) -> None:
         """Order the caller's stream after every queued device->host copy."""
@@ -741,7 +743,10 @@ class RingAttention:
         q_host/k_host/v_host: per-sequence HOST tensors of the new tokens (pinned
         for asynchronous copies).  out_host [S, Hq, D] fp32 / lse_host [S, Hq]
         (pinned) receive this rank's merged result for its S query slots (the
-        rows of ``materialize_rank_block``).  The inputs are staged by
+        rows of ``materialize_rank_block``); or, given as per-sequence LISTS
+        ([new_len_i, Hq, D] / [new_len_i, Hq]), the result in TOKEN order —
+        each rank fills the rows of the tokens it owns (the host-side
+        scatter of ``sharding.unshard``, done by the D2H copies themselves).  The inputs are staged by
         ``stage_host_inputs`` (or taken from ``staged``, queued earlier), every
         ring step runs one attention launch per query range as it lands, and
         each range's final rows go back on a second copy stream as soon as its
@@ -774,14 +779,29 @@ class RingAttention:
         build_kv_message(plan, cache, msg)
         splits = st.splits
 
+        token_order = isinstance(out_host, (list, tuple))
+        if token_order:
+            for sh, o_h, l_h in zip(plan.sequences, out_host, lse_host):
+                if o_h.shape[0] != sh.spec.new_len or l_h.shape[0] != sh.spec.new_len:
+                    raise ValueError(f"sequence {sh.spec.seq_id}: token-order outputs need {sh.spec.new_len} rows")
+
         def on_final(i):
             a, b = splits[i]
             ev = torch.cuda.Event()
             ev.record(cur)
             s_out.wait_event(ev)
             with torch.cuda.stream(s_out):
-                out_host[a:b].copy_(out[a:b], non_blocking=True)
-                lse_host[a:b].copy_(lse[a:b], non_blocking=True)
+                if not token_order:
+                    out_host[a:b].copy_(out[a:b], non_blocking=True)
+                    lse_host[a:b].copy_(lse[a:b], non_blocking=True)
+                    return
+                # token order: every run of consecutive slots of one sequence is
+                # one contiguous run of that sequence's tokens (a chunk), so each
+                # run is one D2H copy straight to its token rows; padding is skipped
+                for j, e, si, lo in _slot_runs(st.idx[a:b], st.seq_off):
+                    if si >= 0:
+                        out_host[si][lo:lo + e - j].copy_(out[a + j:a + e], non_blocking=True)
+                        lse_host[si][lo:lo + e - j].copy_(lse[a + j:a + e], non_blocking=True)
 
         self.pass_kv(st.q, st.qp, st.qs, lay, msg, cfg, out, lse, cache.dtype, q_splits=splits,
                      q_ready=st.q_ready, on_final=on_final)

@@ -139,3 +139,41 @@ def test_staged_pipeline_slot_reuse(ahead):
     torch.cuda.synchronize()
     for i, ((oh, lh), (ro, rl)) in enumerate(zip(outs, refs)):
         assert torch.equal(oh, ro) and torch.equal(lh, rl), i
+
+
+@pytest.mark.parametrize("n_sub", [1, 3])
+def test_host_stream_token_order_outputs(n_sub):
+    """Token-ordered host outputs (per-sequence lists): equal to the device
+    path's slot-ordered result scattered to token order
+    (sharding.scatter_rank_block), bitwise, with ragged fused sequences whose
+    chunks end in padding slots."""
+    from paper_2411_01783_b200.attention import GqaConfig
+    from paper_2411_01783_b200.kv_cache import RankKvCache
+    from paper_2411_01783_b200.ring import RingAttention, _LocalComm
+    from paper_2411_01783_b200.sharding import (SequenceSpec, materialize_rank_block, plan_full_prefill,
+                                                scatter_rank_block)
+
+    hq, hkv, D = 8, 2, 128
+    cfg = GqaConfig(hq, hkv, D)
+    g = torch.Generator().manual_seed(2)
+    lens = [1501, 699]
+    plan = plan_full_prefill([SequenceSpec(3, 0, lens[0]), SequenceSpec(8, 0, lens[1])], 1)
+    mk = lambda *s: torch.randn(*s, generator=g).to(torch.bfloat16).pin_memory()
+    qh, kh, vh = ([mk(n, h, D) for n in lens] for h in (hq, hkv, hkv))
+    ring = RingAttention(_LocalComm(0, 1))
+    ref = ring.pass_kv_prefill(plan, RankKvCache(hkv, D, capacity_tokens=256),
+                               materialize_rank_block(plan, 0, [t.cuda() for t in qh]),
+                               materialize_rank_block(plan, 0, [t.cuda() for t in kh]),
+                               materialize_rank_block(plan, 0, [t.cuda() for t in vh]), cfg)
+    want_o = [torch.empty(n, hq, D, device="cuda") for n in lens]
+    want_l = [torch.empty(n, hq, device="cuda") for n in lens]
+    scatter_rank_block(plan, 0, ref.output.data, want_o)
+    scatter_rank_block(plan, 0, ref.lse, want_l)
+    out_h = [torch.full((n, hq, D), float("nan")).pin_memory() for n in lens]
+    lse_h = [torch.full((n, hq), float("nan")).pin_memory() for n in lens]
+    ring.pass_kv_prefill_host(plan, RankKvCache(hkv, D, capacity_tokens=256), qh, kh, vh, cfg, out_h, lse_h,
+                              n_sub=n_sub)
+    torch.cuda.synchronize()
+    for i in range(2):
+        assert torch.equal(out_h[i], want_o[i].cpu())
+        assert torch.equal(lse_h[i], want_l[i].cpu())

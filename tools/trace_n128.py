@@ -68,3 +68,14 @@ if os.environ.get("RCP_ATTN_VERSION") == "13":
               f"handoff wait {np.mean(g0[:, 10] - g0[:, 9]):.0f}, fixups+tail {np.mean(g0[:, 3] - g0[:, 10]):.0f}")
         its = np.arange(8, 56, 2)
         print(f"  leader: P0(it) arrive -> PV(it) issued {np.mean(d[its, 0] - d[its // 2, 3]):.0f}")
+
+if os.environ.get("RCP_ATTN_VERSION") == "14":
+    # v14 events (per block it): 0 PV issued, 1 S(it+3) issued (leader); 2/4 S seen by group 0/1,
+    # 9 exps done (group 0), 3/5 P arrive of group 0/1
+    for cta in (0, 2):
+        d = t[cta, 8:60]
+        print(f"v14 pair {cta // 2}: cycles per 128-key block {np.mean(np.diff(d[:, 0])):.0f} (tensor ideal 1024 per SM)")
+        print(f"  group 0: S seen -> exps done {np.mean(d[:, 9] - d[:, 2]):.0f}, exps done -> P arrive "
+              f"{np.mean(d[:, 3] - d[:, 9]):.0f}, P arrive -> next S seen {np.mean(d[1:, 2] - d[:-1, 3]):.0f}")
+        print(f"  group 1: S seen -> P arrive {np.mean(d[:, 5] - d[:, 4]):.0f}; leader P -> PV issued "
+              f"{np.mean(d[:, 0] - np.maximum(d[:, 3], d[:, 5])):.0f}")
