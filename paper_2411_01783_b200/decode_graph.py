@@ -55,12 +55,14 @@ class GraphedDecode:
     """
 
     def __init__(self, comm, cache: RankKvCache, cfg: GqaConfig, batch, max_steps: int = 256,
-                 first_iteration: int = 0, first_positions=None, merge_order: str = "arrival"):
+                 first_iteration: int = 0, first_positions=None, merge_order: str = "arrival",
+                 grouped_a2a: bool = True):
         if cache.device.type != "cuda":
             raise RuntimeError("GraphedDecode needs the cache on a CUDA device")
         self.comm, self.cache, self.cfg = comm, cache, cfg
         merge_order_of(0, 1, merge_order)  # validates the mode
         self.merge_mode = merge_order
+        self.grouped_a2a = grouped_a2a
         self.batch = [int(b) for b in batch]
         self.n, self.rank = comm.world, comm.rank
         self.it = int(first_iteration)
@@ -177,8 +179,17 @@ class GraphedDecode:
         d.all_gather_into_tensor(self.q_all, self.q_in, group=self.comm.group)
         _cuda_decode(self.q_all, c.k, c.v, starts, lens, self.max_len, self.cfg, self.part_o, self.part_l,
                      self.ws)
-        d.all_to_all_single(self.recv_o, self.part_o, group=self.comm.group)
-        d.all_to_all_single(self.recv_l, self.part_l, group=self.comm.group)
+        if self.grouped_a2a:
+            # both All2Alls (partial O and LSE) as ONE grouped set of NCCL
+            # send/recv pairs: one NCCL launch per step instead of two
+            so = [self.part_o[s * S:(s + 1) * S] for s in range(self.n)]
+            sl = [self.part_l[s * S:(s + 1) * S] for s in range(self.n)]
+            ro = [self.recv_o[s * S:(s + 1) * S] for s in range(self.n)]
+            rl = [self.recv_l[s * S:(s + 1) * S] for s in range(self.n)]
+            self.comm.wait(self.comm.all_to_all_many([(so, ro), (sl, rl)]))
+        else:
+            d.all_to_all_single(self.recv_o, self.part_o, group=self.comm.group)
+            d.all_to_all_single(self.recv_l, self.part_l, group=self.comm.group)
         order = merge_order_of(self.rank, self.n, self.merge_mode)
         merge_rows_into([self.recv_o[s * S:(s + 1) * S] for s in order],
                         [self.recv_l[s * S:(s + 1) * S] for s in order], self.out, self.lse)

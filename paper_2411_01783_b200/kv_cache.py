@@ -283,6 +283,8 @@ class RankKvCache:
 
     def __del__(self):
         try:
+            if torch.cuda.is_available() and torch.cuda.is_current_stream_capturing():
+                return  # never synchronise inside a graph capture; the reservation is leaked
             self.close()
         except Exception:  # noqa: BLE001 - interpreter shutdown / CUDA already torn down
             pass

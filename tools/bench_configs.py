@@ -192,7 +192,7 @@ def run_decode(args, rank, world):
             # consecutive positions per step: the step metadata is precomputed on the
             # device and selected by the graph (no per-step upload / host metadata)
             gd = GraphedDecode(comm, cache, cfg, batch, max_steps=args.warmup + 2 * args.steps + 4,
-                               first_positions=None if args.no_table else pos0)
+                               first_positions=None if args.no_table else pos0, grouped_a2a=not args.separate_a2a)
 
             def step():  # noqa: F811 - graphed variant
                 it = gd.it
@@ -237,6 +237,8 @@ def main():
     ap.add_argument("--batch", type=int, nargs="*", default=[1, 2, 4, 8, 16, 32])
     ap.add_argument("--gather", action="store_true", help="decode: all-gather Q instead of the Q ring")
     ap.add_argument("--graph", action="store_true", help="decode: replay the step from a CUDA graph")
+    ap.add_argument("--separate-a2a", action="store_true",
+                    help="decode --graph: two All2All collectives instead of one grouped send/recv set")
     ap.add_argument("--no-table", action="store_true",
                     help="decode --graph: upload the step metadata each step instead of the device table")
     ap.add_argument("--calibrate", action="store_true",

@@ -51,7 +51,11 @@ def main():
                 c.append_rows(b, k, v, pos)
         ring = RingAttention(comm)
         steps, warm = 12, 3
-        gd = GraphedDecode(comm, caches[1], cfg, batch, max_steps=2 * (steps + warm) + 4)
+        # GD_TABLE=1: device-resident step table; GD_GROUPED=1: one grouped All2All
+        table = os.environ.get("GD_TABLE") == "1"
+        gd = GraphedDecode(comm, caches[1], cfg, batch, max_steps=2 * (steps + warm) + 4,
+                           first_positions={b: context for b in batch} if table else None,
+                           grouped_a2a=os.environ.get("GD_GROUPED") == "1")
         gq = torch.Generator(device="cuda").manual_seed(7)  # same tokens on every rank
         max_err = 0.0
         t_e, t_g = [], []
@@ -84,7 +88,8 @@ def main():
         stats = torch.tensor([max_err, statistics.median(t_e), statistics.median(t_g)], device="cuda")
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
         if rank == 0:
-            print(f"world {world} B {B} ctx {context}: max |eager - graph| {stats[0].item():.2e}; step eager "
+            print(f"world {world} B {B} ctx {context} table={os.environ.get('GD_TABLE')} "
+                  f"grouped={os.environ.get('GD_GROUPED')}: max |eager - graph| {stats[0].item():.2e}; step eager "
                   f"{stats[1].item():.3f} ms, graph {stats[2].item():.3f} ms", flush=True)
         res.append(stats[0].item())
         del caches, gd
