@@ -424,7 +424,21 @@ def run_ours(args, cfg, rank, world, local_rank):
         barrier()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
         e2e = {"value": flops_total / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-               "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+               "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "out_dtype": "float32"}
+        if args.e2e_bf16:
+            # the same serving loop returning O in the model dtype (bf16, cast on
+            # the device per final range; LSE fp32): half the D2H bytes
+            out_host = torch.empty((s_slots, hq, D), dtype=torch.bfloat16).pin_memory()
+            e2e_steps(2)
+            barrier()
+            e0.record()
+            e2e_steps(args.steps)
+            e1.record()
+            barrier()
+            ms16 = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+            e2e["bf16_out"] = {"value": flops_total / (ms16 * 1e-3) / 1e12, "ms_per_step": ms16,
+                               "d2h_bytes_per_step": out_host.numel() * 2 + lse_host.numel() * 4}
 
     if rank != 0:
         return
@@ -480,6 +494,8 @@ def main():
     ap.add_argument("--seqs", type=int, default=1,
                     help="fused batch: split the tokens into this many ragged sequences (1 : 2 : ... : K)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-bf16", action="store_true",
+                    help="also time the e2e loop with bf16 host outputs (reported under e2e.bf16_out)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=8)
     ap.add_argument("--check", action="store_true",

@@ -123,6 +123,11 @@ int rcp_decode_attn(const void* q, const void* k, const void* v, int64_t kv_row_
                     int64_t max_kv_len, int32_t hq, int32_t hkv, int32_t head_dim, float scale,
                     float* o, float* lse, void* workspace, size_t workspace_bytes, void* stream);
 
+/* fp32 -> bf16 (round to nearest even) of n values (n % 4 == 0): the final
+ * attention output in the model dtype, so the host-buffer path copies half the
+ * bytes back (RingAttention.pass_kv_prefill_host with bf16 host outputs). */
+int rcp_cast_f32_bf16(void* dst, const float* src, int64_t n, void* stream);
+
 /* Decode-graph helper: copy row *counter of the device int64 table
  * [n_rows, row_elems] to dst, then increment *counter (device int64, clamped
  * at n_rows - 1).  GraphedDecode precomputes the per-step metadata of all of

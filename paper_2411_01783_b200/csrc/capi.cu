@@ -305,6 +305,19 @@ __global__ void __launch_bounds__(256) step_select_kernel(int64_t* __restrict__ 
   if (threadIdx.x == 0) *counter = c + 1;
 }
 
+// fp32 -> bf16 (round to nearest even), 4 values per thread: the final
+// attention output in the model dtype for a host copy of half the bytes.
+__global__ void cast_f32_bf16_kernel(const float4* __restrict__ src, uint2* __restrict__ dst, int64_t n4) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 v = __ldg(src + i);
+    uint32_t lo, hi;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(v.y), "f"(v.x));
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(v.w), "f"(v.z));
+    dst[i] = make_uint2(lo, hi);
+  }
+}
+
 static unsigned grid_for(int64_t work, int threads) {
   int64_t b = (work + threads - 1) / threads;
   const int64_t cap = 148 * 16;
@@ -459,6 +472,18 @@ int rcp_shard_scatter(void* const* dst_rows, const void* src, const int64_t* new
   const int64_t vpr = row_bytes / 16;
   shard_scatter_kernel<<<grid_for(slot * 32, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       a, n_seqs, n_ranks, rank, vpr, static_cast<const uint4*>(src));
+  RCP_CUDA(cudaGetLastError());
+  return RCP_OK;
+}
+
+int rcp_cast_f32_bf16(void* dst, const float* src, int64_t n, void* stream) {
+  RCP_CHECK_ARG(n >= 0 && n % 4 == 0, "n must be a non-negative multiple of 4");
+  if (n == 0) return RCP_OK;
+  RCP_CHECK_ARG(dst && src, "null pointer");
+  RCP_CHECK_ARG(((reinterpret_cast<uintptr_t>(src) & 15) | (reinterpret_cast<uintptr_t>(dst) & 7)) == 0,
+                "src must be 16-byte and dst 8-byte aligned");
+  cast_f32_bf16_kernel<<<grid_for(n / 4, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const float4*>(src), static_cast<uint2*>(dst), n / 4);
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
 }

@@ -785,14 +785,26 @@ class RingAttention:
                 if o_h.shape[0] != sh.spec.new_len or l_h.shape[0] != sh.spec.new_len:
                     raise ValueError(f"sequence {sh.spec.seq_id}: token-order outputs need {sh.spec.new_len} rows")
 
+        o_dtype = (out_host[0] if token_order else out_host).dtype
+        if o_dtype not in (torch.float32, torch.bfloat16):
+            raise ValueError("host outputs must be float32 or bfloat16")
+        # bf16 host outputs: each final range is cast on the device (rcp_cast_f32_bf16)
+        # and half the bytes cross PCIe; LSE stays fp32
+        out_src = out if o_dtype == torch.float32 else self._slot_tensor(("out", oslot, "o16"), (S, H, D),
+                                                                          torch.bfloat16, dev)
+
         def on_final(i):
             a, b = splits[i]
+            if out_src is not out:
+                _lib.count("rcp_cast_f32_bf16")
+                _lib.check(_lib.load().rcp_cast_f32_bf16(_lib.ptr(out_src[a:b]), _lib.ptr(out[a:b]),
+                                                         (b - a) * H * D, _lib.stream_handle(cur)))
             ev = torch.cuda.Event()
             ev.record(cur)
             s_out.wait_event(ev)
             with torch.cuda.stream(s_out):
                 if not token_order:
-                    out_host[a:b].copy_(out[a:b], non_blocking=True)
+                    out_host[a:b].copy_(out_src[a:b], non_blocking=True)
                     lse_host[a:b].copy_(lse[a:b], non_blocking=True)
                     return
                 # token order: every run of consecutive slots of one sequence is
@@ -800,7 +812,7 @@ class RingAttention:
                 # run is one D2H copy straight to its token rows; padding is skipped
                 for j, e, si, lo in _slot_runs(st.idx[a:b], st.seq_off):
                     if si >= 0:
-                        out_host[si][lo:lo + e - j].copy_(out[a + j:a + e], non_blocking=True)
+                        out_host[si][lo:lo + e - j].copy_(out_src[a + j:a + e], non_blocking=True)
                         lse_host[si][lo:lo + e - j].copy_(lse[a + j:a + e], non_blocking=True)
 
         self.pass_kv(st.q, st.qp, st.qs, lay, msg, cfg, out, lse, cache.dtype, q_splits=splits,

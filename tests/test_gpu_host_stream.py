@@ -177,3 +177,30 @@ def test_host_stream_token_order_outputs(n_sub):
     for i in range(2):
         assert torch.equal(out_h[i], want_o[i].cpu())
         assert torch.equal(lse_h[i], want_l[i].cpu())
+
+
+def test_host_stream_bf16_outputs():
+    """bf16 host outputs: O is the device fp32 result cast round-to-nearest-even
+    (rcp_cast_f32_bf16), bitwise equal to torch's cast; LSE stays fp32."""
+    from paper_2411_01783_b200.attention import GqaConfig
+    from paper_2411_01783_b200.kv_cache import RankKvCache
+    from paper_2411_01783_b200.ring import RingAttention, _LocalComm
+    from paper_2411_01783_b200.sharding import SequenceSpec, materialize_rank_block, plan_full_prefill
+
+    hq, hkv, D = 8, 2, 128
+    cfg = GqaConfig(hq, hkv, D)
+    g = torch.Generator().manual_seed(3)
+    lens = [1300]
+    plan = plan_full_prefill([SequenceSpec(0, 0, lens[0])], 1)
+    mk = lambda *s: torch.randn(*s, generator=g).to(torch.bfloat16).pin_memory()
+    qh, kh, vh = ([mk(n, h, D) for n in lens] for h in (hq, hkv, hkv))
+    ring = RingAttention(_LocalComm(0, 1))
+    ref = ring.pass_kv_prefill(plan, RankKvCache(hkv, D, capacity_tokens=256),
+                               *(materialize_rank_block(plan, 0, [t.cuda() for t in x]) for x in (qh, kh, vh)), cfg)
+    S = ref.output.n_tokens
+    out_h = torch.empty((S, hq, D), dtype=torch.bfloat16).pin_memory()
+    lse_h = torch.empty((S, hq), dtype=torch.float32).pin_memory()
+    ring.pass_kv_prefill_host(plan, RankKvCache(hkv, D, capacity_tokens=256), qh, kh, vh, cfg, out_h, lse_h, n_sub=2)
+    torch.cuda.synchronize()
+    assert torch.equal(out_h, ref.output.data.to(torch.bfloat16).cpu())
+    assert torch.equal(lse_h, ref.lse.cpu())
