@@ -123,6 +123,35 @@ int rcp_decode_attn(const void* q, const void* k, const void* v, int64_t kv_row_
                     int64_t max_kv_len, int32_t hq, int32_t hkv, int32_t head_dim, float scale,
                     float* o, float* lse, void* workspace, size_t workspace_bytes, void* stream);
 
+/* FP8 KV cache (PAPER.md:393 — beyond the SPEC's bf16
+ * contract, an opt-in RankKvCache(kv_dtype="e4m3") mode).  The arena holds
+ * K/V as OCP e4m3 bytes ([kv_rows, hkv, 128], row stride in elements = bytes)
+ * with one fp32 scale per KV head: value = scale[h] * e4m3.  Same contract as
+ * rcp_decode_attn otherwise (q bf16; o / lse fp32; same workspace size); the
+ * kernel reads half the bytes per key.  Parity: against the decode oracle on
+ * the dequantised K/V, at the bf16 decode tolerance. */
+int rcp_decode_attn_fp8(const void* q, const void* k, const void* v, int64_t kv_row_stride,
+                        int64_t kv_rows, const int64_t* kv_start, const int64_t* kv_len, int64_t batch,
+                        int64_t max_kv_len, int32_t hq, int32_t hkv, int32_t head_dim, float scale,
+                        const float* k_scale, const float* v_scale, float* o, float* lse, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
+/* bf16 rows -> e4m3 rows: row j of src ([n_rows, hkv * head_dim], row stride
+ * in elements) is written to dst row dst_rows[j] (device int64; NULL = row j),
+ * each element satfinite_rn(x / scale[head]) with an IEEE fp32 division
+ * (bit-exact with oracle/ringcp_oracle.py::quantize_e4m3). */
+int rcp_kv_quantize_e4m3(void* dst, int64_t dst_row_stride, const int64_t* dst_rows, const void* src,
+                         int64_t src_row_stride, int64_t n_rows, int32_t hkv, int32_t head_dim,
+                         const float* scale, void* stream);
+/* e4m3 rows -> bf16 rows (x = scale[head] * e4m3 in fp32, rounded to bf16):
+ * snapshots and prefill messages built from an e4m3 cache. */
+int rcp_kv_dequantize_e4m3(void* dst, int64_t dst_row_stride, const void* src, int64_t src_row_stride,
+                           int64_t n_rows, int32_t hkv, int32_t head_dim, const float* scale, void* stream);
+/* Per-KV-head scale from bf16 rows: scale[h] = max(absmax_h, 2^-24) / 448
+ * (fp32 IEEE division).  workspace: hkv * 4 bytes of device memory. */
+int rcp_kv_calibrate_e4m3(const void* src, int64_t src_row_stride, int64_t n_rows, int32_t hkv,
+                          int32_t head_dim, float* scale, void* workspace, void* stream);
+
 /* fp32 -> bf16 (round to nearest even) of n values (n % 4 == 0): the final
  * attention output in the model dtype, so the host-buffer path copies half the
  * bytes back (RingAttention.pass_kv_prefill_host with bf16 host outputs). */

@@ -532,3 +532,79 @@ def sample_rows(n_tokens: int, n_ranks: int, count: int, seed: int = 0) -> np.nd
     while len(rows) < count and len(rows) < n_tokens:
         rows.add(int(rng.integers(0, n_tokens)))
     return np.array(sorted(rows), np.int64)
+
+
+# --------------------------------------------------------------------------- FP8 (e4m3) KV rows
+# Not in the reference (its numerics are fp64 / bf16); the FP8 KV-cache mode is
+# SURVEY §8f rank 4 (FP8 on the attention path).  Restated from
+# the OCP 8-bit floating point spec (E4M3 "fn": bias 7, no infinities,
+# S.1111.111 = NaN, max 448, subnormals m * 2^-9) and the PTX conversion
+# semantics the kernels use (cvt.rn.satfinite.e4m3x2.f32: round to nearest
+# even, |x| > 448 -> 448, NaN -> NaN).  Pinned against torch.float8_e4m3fn in
+# tests/test_oracle_fp8.py.
+E4M3_MAX = 448.0
+
+
+def e4m3_encode(x) -> np.ndarray:
+    """float32 values -> e4m3 bytes (RNE, satfinite)."""
+    v = np.asarray(x, np.float32).astype(np.float64)
+    sign = np.signbit(v).astype(np.uint8) << 7
+    a = np.abs(v)
+    nan = np.isnan(a)
+    a = np.where(nan, 0.0, a)
+    _, ex = np.frexp(np.where(a > 0, a, 1.0))           # a = m * 2^ex, m in [0.5, 1)
+    e = np.maximum(ex - 1, -6)                          # binade (subnormals share 2^-6's quantum)
+    q = np.ldexp(1.0, e - 3)                            # spacing of 3 mantissa bits
+    r = np.minimum(np.rint(a / q) * q, E4M3_MAX)        # RNE, then saturate
+    _, rex = np.frexp(np.where(r > 0, r, 1.0))
+    E = rex - 1
+    normal = r >= 2.0 ** -6
+    man_n = np.rint((r / np.ldexp(1.0, E) - 1.0) * 8).astype(np.int64)
+    bits_n = ((E + 7) << 3) | man_n
+    bits_s = np.rint(r / 2.0 ** -9).astype(np.int64)
+    bits = np.where(normal, bits_n, bits_s).astype(np.uint8)
+    return np.where(nan, np.uint8(0x7F), bits | sign).astype(np.uint8)
+
+
+def e4m3_decode(b) -> np.ndarray:
+    """e4m3 bytes -> float64 values (NaN for S.1111.111)."""
+    b = np.asarray(b, np.uint8).astype(np.int64)
+    s = np.where(b & 0x80, -1.0, 1.0)
+    E = (b >> 3) & 15
+    m = b & 7
+    val = np.where(E == 0, m * 2.0 ** -9, (1.0 + m / 8.0) * np.ldexp(1.0, E - 7))
+    return np.where((b & 0x7F) == 0x7F, np.nan, s * val)
+
+
+def e4m3_scale(rows, n_kv_heads: int) -> np.ndarray:
+    """Per-KV-head calibration scale max(absmax, 2^-24) / 448 in float32
+    (rcp_kv_calibrate_e4m3)."""
+    r = np.asarray(rows, np.float32).reshape(-1, n_kv_heads, np.asarray(rows).shape[-1])
+    amax = np.abs(r).max(axis=(0, 2)) if r.shape[0] else np.zeros(n_kv_heads, np.float32)
+    return (np.maximum(amax, np.float32(2.0 ** -24)).astype(np.float32) / np.float32(E4M3_MAX)).astype(np.float32)
+
+
+def quantize_e4m3(rows, scale) -> np.ndarray:
+    """rows [n, H, D] (float32 / bf16 values) -> e4m3 bytes: RNE(x / scale[h])
+    with the division in IEEE float32 (rcp_kv_quantize_e4m3)."""
+    r = np.asarray(rows, np.float32)
+    s = np.asarray(scale, np.float32).reshape(1, -1, 1)
+    return e4m3_encode((r / s).astype(np.float32))
+
+
+def dequantize_e4m3(bits, scale) -> np.ndarray:
+    """e4m3 bytes [n, H, D] -> exact float64 values scale[h] * e4m3."""
+    return e4m3_decode(bits) * np.asarray(scale, np.float64).reshape(1, -1, 1)
+
+
+def f32_to_bf16_values(x) -> np.ndarray:
+    """Round float32 to bf16 (nearest even), returned as float32 values."""
+    u = np.asarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32)
+
+
+def dequantize_e4m3_bf16(bits, scale) -> np.ndarray:
+    """rcp_kv_dequantize_e4m3: float32(e4m3) * float32(scale) in fp32, rounded to bf16."""
+    v = e4m3_decode(bits).astype(np.float32) * np.asarray(scale, np.float32).reshape(1, -1, 1)
+    return f32_to_bf16_values(v.astype(np.float32))

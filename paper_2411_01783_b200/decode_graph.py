@@ -59,6 +59,8 @@ class GraphedDecode:
                  grouped_a2a: bool = True):
         if cache.device.type != "cuda":
             raise RuntimeError("GraphedDecode needs the cache on a CUDA device")
+        if getattr(cache, "fp8", False) and (cache.k_scale is None or cache.v_scale is None):
+            raise ValueError("e4m3 cache has no k/v scales yet: prefill (or pass scales) before capturing")
         self.comm, self.cache, self.cfg = comm, cache, cfg
         merge_order_of(0, 1, merge_order)  # validates the mode
         self.merge_mode = merge_order
@@ -165,20 +167,20 @@ class GraphedDecode:
                 _lib.ptr(self.meta), _lib.ptr(self._table), self.meta.numel(), _lib.ptr(self._counter),
                 self._table.shape[0], _lib.stream_handle()))
         rows = self.meta[:S]
-        c.k.index_copy_(0, rows, self.k_in)
-        c.v.index_copy_(0, rows, self.v_in)
+        c.store_rows(rows, self.k_in, self.v_in)
         R = self.n * S
         meta32 = self.meta[S + 2 * R:].to(torch.int32)  # pos | seq of the appends
         c.pos.index_copy_(0, rows, meta32[:S])
         c.seq.index_copy_(0, rows, meta32[S:])
         starts, lens = self.meta[S:S + R], self.meta[S + R:S + 2 * R]
         if self.n == 1:
-            _cuda_decode(self.q_in, c.k, c.v, starts, lens, self.max_len, self.cfg, self.out, self.lse, self.ws)
+            _cuda_decode(self.q_in, c.k, c.v, starts, lens, self.max_len, self.cfg, self.out, self.lse, self.ws,
+                         **c.decode_kwargs())
             return
         d = self.comm.dist
         d.all_gather_into_tensor(self.q_all, self.q_in, group=self.comm.group)
         _cuda_decode(self.q_all, c.k, c.v, starts, lens, self.max_len, self.cfg, self.part_o, self.part_l,
-                     self.ws)
+                     self.ws, **c.decode_kwargs())
         if self.grouped_a2a:
             # both All2Alls (partial O and LSE) as ONE grouped set of NCCL
             # send/recv pairs: one NCCL launch per step instead of two

@@ -9,6 +9,14 @@ so decode appends are O(1) and a sequence's history is a single contiguous
 row range — exactly what the decode kernel (rcp_decode_attn) and the ring
 message builder need.
 
+FP8 KV (``kv_dtype="e4m3"``; beyond the SPEC's bf16
+contract): K/V rows are stored as OCP e4m3 bytes with one fp32 scale per KV
+head (value = scale * e4m3; scales given, or calibrated from the first append
+as absmax / 448).  Rows are quantised on the device as they are appended
+(rcp_kv_quantize_e4m3), decode reads them directly (rcp_decode_attn_fp8, half
+the bytes per key), and snapshots / prefill messages dequantise them to bf16
+(rcp_kv_dequantize_e4m3).  ``dtype`` stays the dtype rows are handed out in.
+
 Position bookkeeping lives on the host (every append comes from a plan whose
 positions the host knows, or is checked once), so snapshots and ring messages
 are built without device synchronisation.
@@ -50,7 +58,7 @@ class _VmmArena:
     the existing rows; the base address and the existing data never move."""
 
     _TYPESTR = {torch.bfloat16: ("<i2", 2), torch.int32: ("<i4", 4), torch.float32: ("<f4", 4),
-                torch.int64: ("<i8", 8)}
+                torch.int64: ("<i8", 8), torch.uint8: ("|u1", 1)}
 
     def __init__(self, max_rows: int, row_shape, dtype, device: torch.device):
         import ctypes
@@ -138,15 +146,25 @@ class RankKvCache:
     """``append(seq_id, k_block, v_block) -> cached_len`` and
     ``snapshot_padded(seq_id, max_len) -> (k_block, v_block)`` as in SPEC.md:180-198."""
 
+    KV_DTYPES = ("bf16", "e4m3")
+
     def __init__(self, n_kv_heads: int, head_dim: int, capacity_tokens: int = 1 << 16,
-                 dtype=torch.bfloat16, device=None, growth: str | None = None, max_tokens: int | None = None):
+                 dtype=torch.bfloat16, device=None, growth: str | None = None, max_tokens: int | None = None,
+                 kv_dtype: str = "bf16", k_scale=None, v_scale=None):
         """``growth``: "vmm" (default on CUDA: growable virtual arenas, no copy on
         growth) or "copy" (reallocate by doubling; CPU tensors / tests).
         ``max_tokens`` bounds the VMM reservation (default: what fits in the
-        device's memory)."""
+        device's memory).  ``kv_dtype``: "bf16" or "e4m3" (FP8 storage with
+        per-KV-head ``k_scale`` / ``v_scale``: a float or one per head; None
+        calibrates from the first append)."""
+        if kv_dtype not in self.KV_DTYPES:
+            raise ValueError(f"kv_dtype must be one of {self.KV_DTYPES}, got {kv_dtype!r}")
         self.n_kv_heads = int(n_kv_heads)
         self.head_dim = int(head_dim)
         self.dtype = dtype
+        self.kv_dtype = kv_dtype
+        self.fp8 = kv_dtype == "e4m3"
+        self.storage_dtype = torch.uint8 if self.fp8 else dtype
         self.device = torch.device(device) if device is not None else _device()
         if self.device.type == "cuda" and self.device.index is None:
             self.device = torch.device("cuda", torch.cuda.current_device())
@@ -154,18 +172,24 @@ class RankKvCache:
         if growth is None:
             growth = "vmm" if self.device.type == "cuda" else "copy"
         self.growth = growth
+        self.k_scale = self.v_scale = None
+        if self.fp8:
+            if self.device.type != "cuda" or dtype != torch.bfloat16:
+                raise ValueError("kv_dtype='e4m3' needs a CUDA device and bf16 rows")
+            self.k_scale = self._scale_tensor(k_scale)
+            self.v_scale = self._scale_tensor(v_scale)
         self._free: list[tuple[int, int]] = []  # (start, cap) of evicted segments
         self._used = 0
         self._segs: dict[int, _Segment] = {}
         if growth == "vmm":
-            row = self.n_kv_heads * self.head_dim * torch.tensor([], dtype=dtype).element_size()
+            row = self.n_kv_heads * self.head_dim * torch.tensor([], dtype=self.storage_dtype).element_size()
             if max_tokens is None:
                 total = torch.cuda.get_device_properties(self.device).total_memory
                 max_tokens = total // (2 * row)
             max_tokens = max(int(max_tokens), self._cap)
             self._arenas = {
-                "k": _VmmArena(max_tokens, (n_kv_heads, head_dim), dtype, self.device),
-                "v": _VmmArena(max_tokens, (n_kv_heads, head_dim), dtype, self.device),
+                "k": _VmmArena(max_tokens, (n_kv_heads, head_dim), self.storage_dtype, self.device),
+                "v": _VmmArena(max_tokens, (n_kv_heads, head_dim), self.storage_dtype, self.device),
                 "pos": _VmmArena(max_tokens, (), torch.int32, self.device),
                 "seq": _VmmArena(max_tokens, (), torch.int32, self.device),
             }
@@ -173,7 +197,7 @@ class RankKvCache:
             self._grow_arena(max(int(capacity_tokens), 1))
         else:
             self._arenas = None
-            self.k = torch.zeros((self._cap, n_kv_heads, head_dim), dtype=dtype, device=self.device)
+            self.k = torch.zeros((self._cap, n_kv_heads, head_dim), dtype=self.storage_dtype, device=self.device)
             self.v = torch.zeros_like(self.k)
             self.pos = torch.full((self._cap,), _lib.POS_PAD_K, dtype=torch.int32, device=self.device)
             self.seq = torch.full((self._cap,), _lib.SEQ_PAD_K, dtype=torch.int32, device=self.device)
@@ -211,6 +235,78 @@ class RankKvCache:
             t[: self._used].copy_(old[: self._used])
             setattr(self, name, t)
         self._cap = new_cap
+
+    def _scale_tensor(self, s):
+        if s is None:
+            return None
+        a = np.broadcast_to(np.asarray(s, np.float32).reshape(-1), (self.n_kv_heads,)).copy()
+        if not np.all(np.isfinite(a)) or np.any(a <= 0):
+            raise ValueError("fp8 kv scales must be finite and positive")
+        return torch.from_numpy(a).to(self.device)
+
+    def _calibrate(self, k_rows: torch.Tensor, v_rows: torch.Tensor) -> None:
+        """Per-KV-head scales absmax / 448 from the first rows appended."""
+        lib = _lib.load()
+        ws = torch.empty(self.n_kv_heads, dtype=torch.int32, device=self.device)
+        for name, rows in (("k_scale", k_rows), ("v_scale", v_rows)):
+            if getattr(self, name) is not None:
+                continue
+            out = torch.empty(self.n_kv_heads, dtype=torch.float32, device=self.device)
+            r = rows.reshape(rows.shape[0], -1).contiguous()
+            _lib.count("rcp_kv_calibrate_e4m3")
+            _lib.check(lib.rcp_kv_calibrate_e4m3(_lib.ptr(r), r.stride(0), r.shape[0], self.n_kv_heads,
+                                                 self.head_dim, _lib.ptr(out), _lib.ptr(ws), _lib.stream_handle()))
+            setattr(self, name, out)
+
+    def _store(self, a: int, n: int, k_rows: torch.Tensor, v_rows: torch.Tensor, rows_d=None) -> None:
+        """Write n K/V rows at arena rows a.. (or at rows_d, device int64)."""
+        if not self.fp8:
+            if rows_d is None:
+                self.k[a:a + n].copy_(k_rows.to(self.dtype))
+                self.v[a:a + n].copy_(v_rows.to(self.dtype))
+            else:
+                self.k.index_copy_(0, rows_d, k_rows.to(self.dtype))
+                self.v.index_copy_(0, rows_d, v_rows.to(self.dtype))
+            return
+        if self.k_scale is None or self.v_scale is None:
+            self._calibrate(k_rows, v_rows)
+        lib = _lib.load()
+        row = self.n_kv_heads * self.head_dim
+        for arena, rows, scale in ((self.k, k_rows, self.k_scale), (self.v, v_rows, self.v_scale)):
+            src = rows.to(torch.bfloat16).reshape(n, row).contiguous()
+            dst = arena.data_ptr() + (0 if rows_d is not None else a * row)
+            _lib.count("rcp_kv_quantize_e4m3")
+            _lib.check(lib.rcp_kv_quantize_e4m3(dst, row, _lib.ptr(rows_d), _lib.ptr(src), row, n,
+                                                self.n_kv_heads, self.head_dim, _lib.ptr(scale),
+                                                _lib.stream_handle()))
+
+    def store_rows(self, rows_d: torch.Tensor, k_rows: torch.Tensor, v_rows: torch.Tensor) -> None:
+        """Scatter K/V rows to arena rows ``rows_d`` (device int64) in the
+        cache's storage format (graph-capturable: no host work)."""
+        self._store(0, int(rows_d.shape[0]), k_rows, v_rows, rows_d)
+
+    def load_rows(self, start: int, n: int, k_out: torch.Tensor, v_out: torch.Tensor) -> None:
+        """Copy arena rows [start, start+n) as ``dtype`` rows into k_out / v_out
+        ([n, H, D] views; e4m3 rows are dequantised)."""
+        if n == 0:
+            return
+        if not self.fp8:
+            k_out.copy_(self.k[start:start + n])
+            v_out.copy_(self.v[start:start + n])
+            return
+        lib = _lib.load()
+        row = self.n_kv_heads * self.head_dim
+        for arena, out, scale in ((self.k, k_out, self.k_scale), (self.v, v_out, self.v_scale)):
+            if out.dtype != torch.bfloat16 or out.stride(0) != row or out.stride(-1) != 1:
+                raise ValueError("fp8 rows dequantise into contiguous bf16 [n, H, D] rows")
+            _lib.count("rcp_kv_dequantize_e4m3")
+            _lib.check(lib.rcp_kv_dequantize_e4m3(_lib.ptr(out), row, arena.data_ptr() + start * row, row, n,
+                                                  self.n_kv_heads, self.head_dim, _lib.ptr(scale),
+                                                  _lib.stream_handle()))
+
+    def decode_kwargs(self) -> dict:
+        """Extra arguments of the decode kernel call for this cache's format."""
+        return {"scales": (self.k_scale, self.v_scale)} if self.fp8 else {}
 
     def _reserve(self, seq_id: int, extra: int) -> _Segment:
         seg = self._segs.get(seq_id)
@@ -368,8 +464,7 @@ class RankKvCache:
             seg.max_pos = int(pos[j])
         rows_d = _lib.h2d(rows, self.device)
         meta_d = _lib.h2d(np.stack([pos, np.asarray(ids, np.int64)]).astype(np.int32), self.device)
-        self.k.index_copy_(0, rows_d, k_rows.to(self.dtype))
-        self.v.index_copy_(0, rows_d, v_rows.to(self.dtype))
+        self._store(0, n, k_rows, v_rows, rows_d)
         self.pos.index_copy_(0, rows_d, meta_d[0])
         self.seq.index_copy_(0, rows_d, meta_d[1])
 
@@ -384,8 +479,7 @@ class RankKvCache:
             pos_dev = None if pos_dev is None else pos_dev[sel]
         seg = self._reserve(seq_id, n)
         a = seg.start + seg.length
-        self.k[a:a + n].copy_(k_rows.to(self.dtype))
-        self.v[a:a + n].copy_(v_rows.to(self.dtype))
+        self._store(a, n, k_rows, v_rows)
         if pos_dev is not None:
             self.pos[a:a + n].copy_(pos_dev)
         else:
@@ -412,8 +506,7 @@ class RankKvCache:
         dev = self.device
         kd = torch.zeros((max_len, self.n_kv_heads, self.head_dim), dtype=self.dtype, device=dev)
         vd = torch.zeros_like(kd)
-        kd[:length].copy_(self.k[start:start + length])
-        vd[:length].copy_(self.v[start:start + length])
+        self.load_rows(start, length, kd[:length], vd[:length])
         pos = torch.full((max_len,), -1, dtype=torch.int64, device=dev)
         pos[:length].copy_(self.pos[start:start + length].to(torch.int64))
         valid = torch.zeros(max_len, dtype=torch.bool, device=dev)

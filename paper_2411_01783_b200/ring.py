@@ -324,8 +324,7 @@ def build_kv_message(plan: ShardPlan, cache: RankKvCache, buf: torch.Tensor | No
         if n > L:
             raise ValueError(f"sequence {sh.spec.seq_id}: cache holds {n} rows > L^i = {L}")
         if n:
-            k[off:off + n].copy_(cache.k[start:start + n])
-            v[off:off + n].copy_(cache.v[start:start + n])
+            cache.load_rows(start, n, k[off:off + n], v[off:off + n])
             pos[off:off + n].copy_(cache.pos[start:start + n])
             seq[off:off + n].copy_(cache.seq[start:start + n])
         if L > n:
@@ -504,13 +503,24 @@ def _cuda_merge(o_parts, l_parts, out, lse):
     merge_rows_into(o_parts, l_parts, out, lse)
 
 
-def _cuda_decode(q, k_arena, v_arena, starts, lens, max_len, cfg: GqaConfig, out, lse, ws=None):
-    """Split-KV decode of q [B, Hq, D] against arena rows [starts[b], starts[b]+lens[b])."""
+def _cuda_decode(q, k_arena, v_arena, starts, lens, max_len, cfg: GqaConfig, out, lse, ws=None, scales=None):
+    """Split-KV decode of q [B, Hq, D] against arena rows [starts[b], starts[b]+lens[b]).
+    e4m3 arenas (uint8) take ``scales`` = (k_scale, v_scale) per KV head."""
     lib = _lib.load()
     B, H, D = q.shape
     need = lib.rcp_decode_workspace_bytes(B, H, max(max_len, 1))
     if ws is None or ws.numel() < need:
         ws = torch.empty(max(need, 32), dtype=torch.uint8, device=q.device)
+    if k_arena.dtype == torch.uint8:
+        if scales is None or scales[0] is None or scales[1] is None:
+            raise ValueError("e4m3 kv arenas need (k_scale, v_scale)")
+        _lib.count("rcp_decode_attn_fp8")
+        _lib.check(lib.rcp_decode_attn_fp8(
+            _lib.ptr(q), _lib.ptr(k_arena), _lib.ptr(v_arena), k_arena.stride(0), k_arena.shape[0],
+            _lib.ptr(starts), _lib.ptr(lens), B, max(max_len, 1), H, cfg.n_kv_heads, D, float(cfg.scale),
+            _lib.ptr(scales[0]), _lib.ptr(scales[1]), _lib.ptr(out), _lib.ptr(lse), _lib.ptr(ws), ws.numel(),
+            _lib.stream_handle()))
+        return
     _lib.count("rcp_decode_attn")
     _lib.check(lib.rcp_decode_attn(
         _lib.ptr(q), _lib.ptr(k_arena), _lib.ptr(v_arena), k_arena.stride(0), k_arena.shape[0],
@@ -1015,7 +1025,7 @@ class RingAttention:
                     self.trace.add(step, k, "Q", qlay.nbytes)
             q_cur, _, _ = qlay.views(cur)
             self.decode(q_cur, cache.k, cache.v, st_d[step], ln_d[step], max_len, cfg,
-                        send_o[src], send_l[src])
+                        send_o[src], send_l[src], **cache.decode_kwargs())
             self.comm.wait(works)
             cur = nxt
         recv_o = [torch.empty_like(send_o[0]) for _ in range(n)]
@@ -1055,7 +1065,8 @@ class RingAttention:
         part_o = torch.empty((n * slots, H, D), dtype=torch.float32, device=dev)
         part_l = torch.empty((n * slots, H), dtype=torch.float32, device=dev)
         self.comm.wait(wq)
-        self.decode(q_all, cache.k, cache.v, meta_d[0], meta_d[1], max_len, cfg, part_o, part_l)
+        self.decode(q_all, cache.k, cache.v, meta_d[0], meta_d[1], max_len, cfg, part_o, part_l,
+                    **cache.decode_kwargs())
         recv_o = torch.empty_like(part_o)
         recv_l = torch.empty_like(part_l)
         so = [part_o[s * slots:(s + 1) * slots] for s in range(n)]
@@ -1188,7 +1199,6 @@ def ring_pass_q_decode(plan: DecodePlan, caches: list, q_tok: torch.Tensor, k_to
         caches[plan.owner(b)].append_rows(sid, k_tok[b:b + 1], v_tok[b:b + 1], [int(positions[b])])
     H, D = cfg.n_query_heads, cfg.head_dim
     dev = caches[0].device
-    lib = _lib.load()
     qb = _bf16(q_tok).contiguous()
     out = torch.empty((B, H, D), dtype=torch.float32, device=dev)
     lse = torch.empty((B, H), dtype=torch.float32, device=dev)
@@ -1202,14 +1212,8 @@ def ring_pass_q_decode(plan: DecodePlan, caches: list, q_tok: torch.Tensor, k_to
             ln = torch.tensor([length], dtype=torch.int64, device=dev)
             o = torch.empty((1, H, D), dtype=torch.float32, device=dev)
             l = torch.empty((1, H), dtype=torch.float32, device=dev)
-            ws_bytes = lib.rcp_decode_workspace_bytes(1, H, max(length, 1))
-            ws = torch.empty(max(ws_bytes, 32), dtype=torch.uint8, device=dev)
-            _lib.count("rcp_decode_attn")
-            _lib.check(lib.rcp_decode_attn(
-                _lib.ptr(qb[b:b + 1]), _lib.ptr(caches[s].k), _lib.ptr(caches[s].v), caches[s].k.stride(0),
-                caches[s].k.shape[0],
-                _lib.ptr(st), _lib.ptr(ln), 1, max(length, 1), H, cfg.n_kv_heads, D, float(cfg.scale),
-                _lib.ptr(o), _lib.ptr(l), _lib.ptr(ws), ws.numel(), _lib.stream_handle()))
+            _cuda_decode(qb[b:b + 1], caches[s].k, caches[s].v, st, ln, length, cfg, o, l,
+                         **caches[s].decode_kwargs())
             parts_o.append(o)
             parts_l.append(l)
         _cuda_merge(parts_o, parts_l, out[b:b + 1], lse[b:b + 1])

@@ -159,7 +159,7 @@ def run_decode(args, rank, world):
     ring = RingAttention(comm)
     local = args.context // world
     for B in args.batch:
-        cache = RankKvCache(hkv, D, capacity_tokens=B * (local + 128))
+        cache = RankKvCache(hkv, D, capacity_tokens=B * (local + 128), kv_dtype=args.kv_dtype)
         batch = list(range(B))
         hplan = plan_full_prefill([SequenceSpec(0, 0, args.context)], world)
         loc = hplan.rank_local_indices(0, rank)
@@ -215,13 +215,14 @@ def run_decode(args, rank, world):
             e.record()
             torch.cuda.synchronize()
             b2b = max_over_ranks(s.elapsed_time(e) / nb, world)
-        kv_bytes = B * local * hkv * D * 2 * 2  # this rank's K+V read per decode step
+        elem = 1 if args.kv_dtype == "e4m3" else 2
+        kv_bytes = B * local * hkv * D * 2 * elem  # this rank's K+V read per decode step
         if rank == 0:
             print(json.dumps({
                 "config": "cfg5-ring-pass-q-decode", "cp": world, "batch": B, "context": args.context,
                 "q_transport": "allgather" if (args.gather or args.graph) else "ring",
                 "cuda_graph": bool(args.graph), "device_step_table": bool(args.graph and not args.no_table),
-                "n_q_heads": hq, "n_kv_heads": hkv, "step_ms": ms, "step_ms_back_to_back": b2b,
+                "n_q_heads": hq, "n_kv_heads": hkv, "kv_dtype": args.kv_dtype, "step_ms": ms, "step_ms_back_to_back": b2b,
                 "kv_bytes_per_rank": kv_bytes, "hbm_gbs_effective": kv_bytes / (ms * 1e-3) / 1e9}), flush=True)
         del cache
         torch.cuda.empty_cache()
@@ -245,6 +246,8 @@ def main():
                     help="partial: feed Alg. 1 the attention / link / All2All constants measured in this run")
     ap.add_argument("--fused", action="store_true",
                     help="partial: also time pass-Q with peer-memory partials (no All2All), checked bitwise")
+    ap.add_argument("--kv-dtype", choices=["bf16", "e4m3"], default="bf16",
+                    help="decode: KV-cache storage (e4m3 = FP8 KV, per-head scales calibrated at prefill)")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     args = ap.parse_args()
