@@ -501,8 +501,12 @@ __global__ void __launch_bounds__(kCombineWarps * 32) decode_combine_kernel(
 #ifndef RCP_DEC_CTA_TARGET
 #define RCP_DEC_CTA_TARGET (148 * 8)
 #endif
+// e4m3: a CTA streams half the bytes per key, so fewer, longer CTAs: 148 x 6
+// (two full waves of three CTAs per SM at B = 1) measured 0.113 ms per B = 1
+// kernel (262144 keys x 8 KV heads) against 0.132 ms at 148 x 8, and 0.41 vs
+// 0.47 ms at B = 4 (profiles/r02_decode_kernel_sweep.jsonl).
 #ifndef RCP_DEC_CTA_TARGET_FP8
-#define RCP_DEC_CTA_TARGET_FP8 (148 * 8)
+#define RCP_DEC_CTA_TARGET_FP8 (148 * 6)
 #endif
 // Batch rows counted by the split heuristic: the all-gathered decode form
 // launches N x slots query rows of which, at small batch, only ~1/N are

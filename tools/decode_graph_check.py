@@ -41,7 +41,9 @@ def main():
         loc = hplan.rank_local_indices(0, rank)
         pos = loc[loc >= 0]
         local_len = len(pos)
-        caches = [RankKvCache(hkv, D, capacity_tokens=B * (local_len + 128)) for _ in range(2)]
+        # GD_KV=e4m3: FP8 KV caches (scales calibrated by the identical first appends)
+        caches = [RankKvCache(hkv, D, capacity_tokens=B * (local_len + 128), kv_dtype=os.environ.get("GD_KV", "bf16"))
+                  for _ in range(2)]
         g = torch.Generator(device="cuda").manual_seed(100 + rank)
         for b in batch:
             k = torch.randn(local_len, hkv, D, device="cuda", dtype=torch.bfloat16, generator=g)
@@ -88,7 +90,7 @@ def main():
         stats = torch.tensor([max_err, statistics.median(t_e), statistics.median(t_g)], device="cuda")
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
         if rank == 0:
-            print(f"world {world} B {B} ctx {context} table={os.environ.get('GD_TABLE')} "
+            print(f"world {world} B {B} ctx {context} kv={os.environ.get('GD_KV', 'bf16')} table={os.environ.get('GD_TABLE')} "
                   f"grouped={os.environ.get('GD_GROUPED')}: max |eager - graph| {stats[0].item():.2e}; step eager "
                   f"{stats[1].item():.3f} ms, graph {stats[2].item():.3f} ms", flush=True)
         res.append(stats[0].item())
