@@ -186,6 +186,24 @@ def cpu_baseline_port(T, hq, hkv, rows=16):
                       f"oracle gqa {dt:.2f} s"}
 
 
+def ragged_seq_lens(T: int, K: int) -> list:
+    """A fused batch of K sequences splitting T tokens (lengths ~ 1 : 2 : ... : K)."""
+    w = np.arange(1, K + 1, dtype=np.float64)
+    lens = np.floor(T * w / w.sum()).astype(np.int64)
+    lens[-1] += T - int(lens.sum())
+    return [int(x) for x in lens]
+
+
+def workload_config(cfg, world: int, K: int) -> dict:
+    """The `config` object of both arms' JSON lines (identical by construction)."""
+    T, hq, hkv = cfg["T"], cfg["hq"], cfg["hkv"]
+    return {"workload": cfg["workload"], "seq_len": T, "n_q_heads": hq, "n_kv_heads": hkv,
+            "head_dim": D, "cp": world, "protocol": "pass_kv", "parallelism": f"cp{world}",
+            "sequences": K, **({"seq_lens": ragged_seq_lens(T, K)} if K > 1 else {}),
+            "l2": "inputs larger than L2 (Q %.0f MB, K/V %.0f MB per rank)" % (
+                T // world * hq * D * 2 / 1e6, T // world * hkv * D * 2 / 1e6)}
+
+
 def run_reference(args, cfg, rank, world):
     """--impl reference: the reference algorithm (oracle port; the reference is
     pure Python/numpy) on the host cores, rank 0 only."""
@@ -203,7 +221,7 @@ def run_reference(args, cfg, rank, world):
     rows_per, head_stride = (2, 1) if short else (1, hq // hkv)
     jobs = [(T, hq, hkv, rows_per, 100 + i, head_stride) for i in range(cores)]
     ctx = mp.get_context("fork")
-    vals = []
+    vals, step_ms = [], []
     with ctx.Pool(cores) as pool:
         for it in range(args.warmup + args.steps):
             t0 = time.perf_counter()
@@ -212,14 +230,19 @@ def run_reference(args, cfg, rank, world):
             triples = sum(r[1] for r in res)
             if it >= args.warmup:
                 vals.append(4.0 * D * triples / dt / 1e12)
+                step_ms.append(dt * 1e3)
     value = statistics.median(vals)
+    full_flops = 4.0 * D * hq * sum(L * (L + 1) // 2 for L in ragged_seq_lens(T, max(1, args.seqs)))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        # each timed step is a bounded SAMPLE of the workload (the full step
+        # would take hours on the host cores); ms_per_step is the sample's
+        # wall time, full_step_projected_s the whole workload at this rate
+        "ms_per_step": statistics.median(step_ms), "full_step_projected_s": full_flops / (value * 1e12),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "seq_len": T, "n_q_heads": hq, "n_kv_heads": hkv,
-                   "head_dim": D, "cp": world},
+        "config": workload_config(cfg, world, max(1, args.seqs)),
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
                          "sample": f"{cores} processes x {rows_per} query rows x {T} keys x "
                                    f"{len(range(0, hq, head_stride))} query heads per step"},
@@ -247,10 +270,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     # a fused batch of --seqs sequences splits the T tokens into ragged
     # sequences (lengths ~ 1 : 2 : ... : K); the default is one sequence
     K = max(1, args.seqs)
-    w = np.arange(1, K + 1, dtype=np.float64)
-    seq_lens = np.floor(T * w / w.sum()).astype(np.int64)
-    seq_lens[-1] += T - int(seq_lens.sum())
-    seq_lens = [int(x) for x in seq_lens]
+    seq_lens = ragged_seq_lens(T, K)
     seq_off = np.concatenate([[0], np.cumsum(seq_lens)]).astype(np.int64)
     plan = plan_full_prefill([SequenceSpec(i, 0, L) for i, L in enumerate(seq_lens)], world)
 
@@ -461,11 +481,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic",
-        "config": {"workload": cfg["workload"], "seq_len": T, "n_q_heads": hq, "n_kv_heads": hkv,
-                   "head_dim": D, "cp": world, "protocol": "pass_kv", "parallelism": f"cp{world}",
-                   "sequences": K, **({"seq_lens": seq_lens} if K > 1 else {}),
-                   "l2": "inputs larger than L2 (Q %.0f MB, K/V %.0f MB per rank)" % (
-                       T // world * hq * D * 2 / 1e6, T // world * hkv * D * 2 / 1e6)},
+        "config": workload_config(cfg, world, K),
         "latency_ms": ms, "tflops_per_gpu": value / world,
         "roofline": {"bound": "tensor", "kernel": "attn_fwd_kernel", "achieved": achieved,
                      "peak": pk["bf16_sus"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_sus"],
