@@ -155,7 +155,7 @@ __device__ __forceinline__ float2 ex2_poly_x2(float a, float b) {
 // 128-key blocks, one S buffer per tile.  v13 (attn_fwd_pair.cu): CTA pairs,
 // 128-key blocks, three S buffers, block-alternating softmax groups.
 // Key-block rows of a version's tile summaries:
-inline int attn_key_rows(int version) { return version == 4 ? 64 : 128; }
+inline int attn_key_rows(int version) { return (version == 4 || version == 15) ? 64 : 128; }
 // TMA box rows of the K / V maps (v13 loads half blocks: 64 keys of K, 128 keys x 64 dims of V)
 inline int attn_k_box_rows(int version) { return (version == 13 || version == 14) ? 64 : attn_key_rows(version); }
 inline int attn_v_box_rows(int version) { return attn_key_rows(version); }

@@ -93,6 +93,12 @@ __global__ void __launch_bounds__(256) active_list_kernel(const TileSum* __restr
   if (qb == 0 && threadIdx.x == 0) act_n[gridDim.x] = 0;  // v9's work-item counter (workspace slack)
 }
 
+// kPhase (v15, RCP_ATTN_VERSION=15): the two tiles' softmax warps that share
+// an SMSP (warps 4+s and 8+s) run half a block apart — tile 1 starts block j
+// once tile 0 has its block-j max, tile 0 starts block j+1 once tile 1 has its
+// block-j max (two named barriers per SMSP pair) — so one warp's TMEM load,
+// row max and P store overlap the other's exps instead of coinciding.
+template <int kPhase>
 __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
@@ -273,10 +279,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     const int n = __ldg(p.act_n + qblk);
     const uint32_t* act = p.act + static_cast<int64_t>(qblk) * p.n_kblocks;
     uint32_t e_next = n > 0 ? __ldg(act) : 0u;
+    const uint32_t id_ab = 1 + (warp & 3), id_ba = 5 + (warp & 3);  // kPhase: tile 0 -> 1, 1 -> 0
     int it = 0;
     for (; it < n; ++it) {
       const int buf = it & 1;
       const uint32_t s_addr = lane_base + kTmemS + (2 * w + buf) * kKRows;
+      if constexpr (kPhase != 0) {
+        if (w == 1)
+          named_bar_sync(id_ab, 64);  // tile 0 has the max of block it
+        else if (it > 0)
+          named_bar_sync(id_ba, 64);  // tile 1 has the max of block it - 1
+      }
       const uint32_t e = e_next;
       if (it + 1 < n) e_next = __ldg(act + it + 1);
       const int j = act_j(e);
@@ -333,6 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         // tcgen05.ld/st are .sync.aligned).
         const float m_use = (m == -INFINITY) ? 0.f : m;
         const uint64_t negm2 = f2(-m_use, -m_use);
+        if constexpr (kPhase != 0) named_bar_arrive(w == 0 ? id_ab : id_ba, 64);
         if (t == 0 && w == 0) TRACE(9, it);
         uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
         uint32_t pk[32];
@@ -388,6 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
           }
         }
       } else {
+        if constexpr (kPhase != 0) named_bar_arrive(w == 0 ? id_ab : id_ba, 64);
         uint32_t pk[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) pk[i] = 0u;
@@ -403,6 +418,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       mbar_arrive(&bar_p[w][buf]);
     }
 
+    if constexpr (kPhase != 0) {
+      if (w == 0 && n > 0) named_bar_sync(id_ba, 64);  // consume tile 1's last arrival
+    }
     // epilogue: O / l, LSE, optional merge into the running (O, LSE)
     if (it > 0) {
       mbar_wait(&bar_o[w], 0);
@@ -568,7 +586,7 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
   if (version < 0) {
     const char* e = getenv("RCP_ATTN_VERSION");
     const int v = e ? atoi(e) : kDefaultAttnVersion;
-    version = (v == 4 || v == 12 || v == 13 || v == 14) ? v : kDefaultAttnVersion;
+    version = (v == 4 || v == 12 || v == 13 || v == 14 || v == 15) ? v : kDefaultAttnVersion;
   }
   const int krows = attn_key_rows(version);
   AttnParams prm;
@@ -632,11 +650,16 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
   } else {
     static bool attr_set = false;
     if (!attr_set) {
-      RCP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      RCP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kSmemBytes));
+      RCP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     kSmemBytes));
       attr_set = true;
     }
-    attn_fwd_kernel<<<static_cast<unsigned>(grid), kThreads, kSmemBytes, st>>>(prm);
+    if (version == 15)
+      attn_fwd_kernel<1><<<static_cast<unsigned>(grid), kThreads, kSmemBytes, st>>>(prm);
+    else
+      attn_fwd_kernel<0><<<static_cast<unsigned>(grid), kThreads, kSmemBytes, st>>>(prm);
   }
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
