@@ -93,6 +93,16 @@ __global__ void __launch_bounds__(256) active_list_kernel(const TileSum* __restr
   if (qb == 0 && threadIdx.x == 0) act_n[gridDim.x] = 0;  // v9's work-item counter (workspace slack)
 }
 
+// Bound-finding knobs (tools/dbg_builds.sh builds them into separate .so
+// files; never set in the product build): RCP_DBG_S_STEPS < 8 computes S over
+// fewer K-dim steps, RCP_DBG_NO_EXP replaces the exponentials by a copy.
+#ifndef RCP_DBG_S_STEPS
+#define RCP_DBG_S_STEPS (kD / 16)
+#endif
+#ifndef RCP_DBG_NO_EXP
+#define RCP_DBG_NO_EXP 0
+#endif
+
 // kPhase (v15, RCP_ATTN_VERSION=15): the two tiles' softmax warps that share
 // an SMSP (warps 4+s and 8+s) run half a block apart — tile 1 starts block j
 // once tile 0 has its block-j max, tile 0 starts block j+1 once tile 1 has its
@@ -212,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         const uint32_t ka = k_lo + (((ld % kSlots) * kKVBytes) >> 4);
         const uint32_t d = tmem + kTmemS + (2 * tt + buf) * kKRows;
 #pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk)
+        for (int kk = 0; kk < RCP_DBG_S_STEPS; ++kk)
           mma_ss_lo(d, qa + (((kk >> 2) * kQBoxBytes + (kk & 3) * 32) >> 4),
                     ka + (((kk >> 2) * kKVBoxBytes + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
       };
@@ -355,7 +365,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
           for (int i = 0; i < 32; ++i) {
             const float2 x = unf2(ffma2(f2(s[2 * i], s[2 * i + 1]), sl2x2, negm2));
             float p0, p1;
-            if ((i & 7) < kPolyPairsPer8) {
+            if (RCP_DBG_NO_EXP) {  // bound-finding builds only (tools/dbg_builds.sh)
+              p0 = x.x;
+              p1 = x.y;
+            } else if ((i & 7) < kPolyPairsPer8) {
 #if RCP_PACKED_POLY
               const float2 pp = ex2_poly_x2(x.x, x.y);
               p0 = pp.x;
