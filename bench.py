@@ -417,7 +417,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         d2h = out_host.numel() * 4 + lse_host.numel() * 4
 
         def stage():
-            return ring.stage_host_inputs(plan, host["q"], host["k"], host["v"], gcfg, dev)
+            return ring.stage_host_inputs(plan, host["q"], host["k"], host["v"], gcfg, dev, n_sub=args.e2e_ranges)
 
         def e2e_steps(n):
             # public host-buffer API as a serving loop: each request's K/V and
@@ -512,6 +512,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-bf16", action="store_true",
                     help="also time the e2e loop with bf16 host outputs (reported under e2e.bf16_out)")
+    ap.add_argument("--e2e-ranges", type=int, default=None,
+                    help="query ranges per request in the e2e loop (default: the library's, one per 8192 slots, <= 16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=8)
     ap.add_argument("--check", action="store_true",

@@ -671,7 +671,7 @@ class RingAttention:
                           n_sub: int | None = None) -> "HostStage":
         """Queue the host->device copies of one prefill's inputs on the copy
         stream: K/V of this rank's chunks first, then its query slots in ranges
-        (``n_sub``, default one per 8192 slots, at most 16), each range with a
+        (``n_sub``, default one per 8192 slots, at most 4), each range with a
         ready event.  The device buffers are one of two rotating staging slots
         (the copies into a slot wait for the compute that last read it), so
         staging may run one request ahead of the compute stream; the host
@@ -684,7 +684,12 @@ class RingAttention:
         idx, posv, seqv = _host_index_map(plan, k)
         S = idx.shape[0]
         if n_sub is None:
-            n_sub = min(16, max(1, S // 8192))
+            # each range is one attention launch per ring step, whose tail wave
+            # is exposed; in a serving loop the next request is staged while
+            # this one computes, so ranges only pace the D2H stream.  8B 128K
+            # CP1 serving loop: 1110 / 1146 / 1154 / 1142 TF/s e2e with
+            # 16 / 8 / 4 / 2 ranges (profiles/r02_e2e_ranges_cp1.txt)
+            n_sub = min(4, max(1, S // 8192))
         step = max(256, -(-S // max(n_sub, 1)) // 256 * 256)
         splits = [(a, min(S, a + step)) for a in range(0, S, step)]
         q_host, k_host, v_host = ([t if isinstance(t, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(t))
