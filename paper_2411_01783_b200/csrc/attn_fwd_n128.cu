@@ -59,6 +59,12 @@ static_assert(kSmemBytesN <= 232448, "v12 shared memory exceeds 227 KB");
 #endif
 constexpr int kPolyPairsN = RCP_POLY_PAIRS_N;
 
+// kTurn (v16, RCP_ATTN_VERSION=16): the two tiles' softmax warps that share an
+// SMSP take turns on the exponentials (tile 0 block j, tile 1 block j, tile 0
+// block j+1, ...; two named barriers per SMSP pair), so the MUFU / FMA pipes
+// serve one warp at a time and the tiles settle half a period apart — one
+// tile's exps run while the other tile's PV and next S occupy the tensor cores.
+template <bool kTurn>
 __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid_constant__ AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
@@ -206,6 +212,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid
     const uint64_t sl2x2 = f2(sl2, sl2);
     float m = -INFINITY, l = 0.f;
     uint32_t e_next = n > 0 ? __ldg(act) : 0u;
+    const uint32_t id_ab = 1 + (warp & 3), id_ba = 5 + (warp & 3);  // kTurn: tile 0 -> 1, 1 -> 0
+    auto turn_begin = [&](int i) {
+      if constexpr (kTurn) {
+        if (w == 1)
+          named_bar_sync(id_ab, 64);  // tile 0 finished its exps of block i
+        else if (i > 0)
+          named_bar_sync(id_ba, 64);  // tile 1 finished its exps of block i - 1
+      }
+    };
+    auto turn_end = [&]() {
+      if constexpr (kTurn) named_bar_arrive(w == 0 ? id_ab : id_ba, 64);
+    };
     int it = 0;
     for (; it < n; ++it) {
       const uint32_t e = e_next;
@@ -324,17 +342,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid
             tmem_st16(s_addr + 16 * q, pk);
           }
         };
+        turn_begin(it);
         if (cls == kTileFull) {
           exp_chunks(std::true_type{});
         } else {
           exp_chunks(std::false_type{});
         }
+        turn_end();
         if (t == 0 && w == 0) TRACE(10, it);
         const float2 a01 = unf2(fadd2(acc2[0], acc2[1]));
         const float2 a23 = unf2(fadd2(acc2[2], acc2[3]));
         const float sum = (a01.x + a01.y) + (a23.x + a23.y);
         l = (m_old == -INFINITY ? 0.f : l * f) + sum;
       } else {
+        turn_begin(it);
+        turn_end();
         uint32_t pk[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) pk[i] = 0u;
@@ -347,6 +369,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid
       if (t == 0) TRACE(3 + 2 * w, it);
     }
 
+    if constexpr (kTurn) {
+      if (w == 0 && n > 0) named_bar_sync(id_ba, 64);  // consume tile 1's last arrival
+    }
     // epilogue: O / l, LSE, optional merge into the running (O, LSE)
     if (it > 0) {
       mbar_wait(&bar_o[w], 0);
@@ -398,14 +423,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-int attn_n128_launch(const AttnParams& prm, int64_t grid, cudaStream_t st) {
+int attn_n128_launch(const AttnParams& prm, int64_t grid, cudaStream_t st, bool turn) {
   static bool attr_set = false;
   if (!attr_set) {
-    RCP_CUDA(cudaFuncSetAttribute(attn_fwd_n128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RCP_CUDA(cudaFuncSetAttribute(attn_fwd_n128_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemBytesN));
+    RCP_CUDA(cudaFuncSetAttribute(attn_fwd_n128_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kSmemBytesN));
     attr_set = true;
   }
-  attn_fwd_n128_kernel<<<static_cast<unsigned>(grid), kThreads, kSmemBytesN, st>>>(prm);
+  if (turn)
+    attn_fwd_n128_kernel<true><<<static_cast<unsigned>(grid), kThreads, kSmemBytesN, st>>>(prm);
+  else
+    attn_fwd_n128_kernel<false><<<static_cast<unsigned>(grid), kThreads, kSmemBytesN, st>>>(prm);
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
 }
