@@ -343,6 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid
           }
         };
         turn_begin(it);
+        if (t == 0 && w == 0) TRACE(11, it);
         if (cls == kTileFull) {
           exp_chunks(std::true_type{});
         } else {

@@ -44,7 +44,8 @@ for cta in (range(3) if os.environ.get("RCP_ATTN_VERSION") != "13" else []):
     print(f"CTA {cta}: cycles per 128-key block {np.mean(np.diff(s0)):.0f} (tensor ideal 2048 for 2 tiles)")
     print(f"  softmax (S ready -> P arrive): tile0 {np.mean(p0 - s0):.0f}, tile1 {np.mean(p1 - s1):.0f}")
     print(f"  tile0 phases: ld {np.mean(d[:, 8] - s0):.0f}, mask+max {np.mean(d[:, 9] - d[:, 8]):.0f}, "
-          f"exp+st {np.mean(d[:, 10] - d[:, 9]):.0f}, sum+st wait+arrive {np.mean(p0 - d[:, 10]):.0f}")
+          f"turn wait (v16) {np.mean(d[:, 11] - d[:, 9]):.0f}, exp+st {np.mean(d[:, 10] - d[:, 11]):.0f}, "
+          f"sum+st wait+arrive {np.mean(p0 - d[:, 10]):.0f}")
     print(f"  P0 -> PV0 issued {np.mean(d[:, 0] - p0):.0f}; PV0 issued -> S0(+1) issued {np.mean(d[:, 12] - d[:, 0]):.0f}; "
           f"S0(+1) issued -> S0(+1) ready {np.mean(s0[1:] - d[:-1, 12]):.0f}")
     print(f"  P1 -> PV1 issued {np.mean(d[:, 1] - p1):.0f}; PV1 issued -> S1(+1) issued {np.mean(d[:, 13] - d[:, 1]):.0f}; "
