@@ -114,7 +114,8 @@ int rcp_fold_meta(const int64_t* pos, const int64_t* seq, const uint8_t* valid, 
  * [kv_start[b], kv_start[b] + kv_len[b]) of the KV arena k/v ([kv_rows, hkv,
  * 128] bf16, row stride kv_row_stride), all causally visible (the cache holds
  * only the past and the token itself) and of the same sequence.  kv_start /
- * kv_len are device int64 arrays; max_kv_len bounds kv_len.  hq / hkv <= 16.
+ * kv_len are device int64 arrays; max_kv_len bounds kv_len.  Any hq / hkv (16
+ * query heads per CTA; larger groups take several CTAs per KV head).
  * Writes o [B, hq, 128] fp32, lse [B, hq] fp32 (-inf when kv_len == 0).
  * workspace: rcp_decode_workspace_bytes(B, hq, max_kv_len). */
 size_t rcp_decode_workspace_bytes(int64_t batch, int32_t hq, int64_t max_kv_len);

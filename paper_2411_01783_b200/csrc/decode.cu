@@ -164,18 +164,24 @@ __global__ void __launch_bounds__(kDecThreads) decode_mma_kernel(const __grid_co
   // KV heads vary fastest: the CTAs of one key range's heads run together, so
   // the L2 lines they share (e4m3: two heads' rows per 256-byte promotion) are
   // read from DRAM once
-  const int kvh = blockIdx.x, split = blockIdx.y, b = blockIdx.z;
+  // Groups of more than 16 query heads per KV head (MQA-like geometries) take
+  // ceil(group / 16) CTAs per KV head, 16 heads each (the K/V block is then
+  // read once per 16 heads; L2 serves the repeats of CTAs running together).
+  const int n_hc = (p.group + kDecMaxGroup - 1) / kDecMaxGroup;
+  const int kvh = static_cast<int>(blockIdx.x) / n_hc, hc = static_cast<int>(blockIdx.x) - kvh * n_hc;
+  const int grp = min(kDecMaxGroup, p.group - hc * kDecMaxGroup);  // query heads of this CTA
+  const int split = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t4 = lane & 3;
   const int64_t len = __ldg(p.kv_len + b);
   const int64_t k0 = static_cast<int64_t>(split) * p.keys_per_cta;
   const int64_t k1 = min(len, k0 + p.keys_per_cta);
   const int n_blocks = k1 > k0 ? static_cast<int>((k1 - k0 + kDecBlock - 1) / kDecBlock) : 0;
-  const int row0 = b * p.hq + kvh * p.group;  // first query-head row of this GQA group
+  const int row0 = b * p.hq + kvh * p.group + hc * kDecMaxGroup;  // first query-head row of this CTA
   const int64_t part_base = static_cast<int64_t>(row0) * p.n_split + split;
 
   if (n_blocks == 0) {  // empty split: (0, -inf)
-    for (int i = threadIdx.x; i < p.group * 128; i += blockDim.x) {
+    for (int i = threadIdx.x; i < grp * 128; i += blockDim.x) {
       const int h = i >> 7;
       p.part_o[(part_base + static_cast<int64_t>(h) * p.n_split) * 128 + (i & 127)] = 0.f;
       if ((i & 127) == 0) p.part_lse[part_base + static_cast<int64_t>(h) * p.n_split] = -INFINITY;
@@ -209,8 +215,8 @@ __global__ void __launch_bounds__(kDecThreads) decode_mma_kernel(const __grid_co
     for (int ks = 0; ks < 8; ++ks) {
       const int c = ks * 16 + 4 * t4;
       uint2 r0 = make_uint2(0u, 0u), r1 = make_uint2(0u, 0u);
-      if (g < p.group) r0 = *reinterpret_cast<const uint2*>(q0 + g * 128 + c);
-      if (g + 8 < p.group) r1 = *reinterpret_cast<const uint2*>(q0 + (g + 8) * 128 + c);
+      if (g < grp) r0 = *reinterpret_cast<const uint2*>(q0 + g * 128 + c);
+      if (g + 8 < grp) r1 = *reinterpret_cast<const uint2*>(q0 + (g + 8) * 128 + c);
       auto cvt = [](uint32_t b) {
         const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&b));
         return pack_f16x2(f.x, f.y);
@@ -225,10 +231,10 @@ __global__ void __launch_bounds__(kDecThreads) decode_mma_kernel(const __grid_co
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
       const int c = ks * 16 + 2 * t4;
-      qa[ks][0] = g < p.group ? *reinterpret_cast<const uint32_t*>(q0 + g * 128 + c) : 0u;
-      qa[ks][1] = g + 8 < p.group ? *reinterpret_cast<const uint32_t*>(q0 + (g + 8) * 128 + c) : 0u;
-      qa[ks][2] = g < p.group ? *reinterpret_cast<const uint32_t*>(q0 + g * 128 + c + 8) : 0u;
-      qa[ks][3] = g + 8 < p.group ? *reinterpret_cast<const uint32_t*>(q0 + (g + 8) * 128 + c + 8) : 0u;
+      qa[ks][0] = g < grp ? *reinterpret_cast<const uint32_t*>(q0 + g * 128 + c) : 0u;
+      qa[ks][1] = g + 8 < grp ? *reinterpret_cast<const uint32_t*>(q0 + (g + 8) * 128 + c) : 0u;
+      qa[ks][2] = g < grp ? *reinterpret_cast<const uint32_t*>(q0 + g * 128 + c + 8) : 0u;
+      qa[ks][3] = g + 8 < grp ? *reinterpret_cast<const uint32_t*>(q0 + (g + 8) * 128 + c + 8) : 0u;
     }
   }
   float o[16][4];
@@ -421,7 +427,7 @@ __global__ void __launch_bounds__(kDecThreads) decode_mma_kernel(const __grid_co
     __syncthreads();
   }
   const float vsc = kFp8 ? __ldg(p.v_scale + kvh) : 1.f;
-  for (int i = threadIdx.x; i < p.group * 128; i += blockDim.x) {
+  for (int i = threadIdx.x; i < grp * 128; i += blockDim.x) {
     const int h = i >> 7;
     float L = 0.f, mm = red_m[0][h];
     for (int w2 = 0; w2 < kDecWarps; ++w2) L += red_l[w2][h];
@@ -614,7 +620,6 @@ static int decode_launch(const void* q, const void* k, const void* v, int64_t kv
   RCP_CHECK_ARG(head_dim == 128, "head_dim must be 128, got %d", head_dim);
   RCP_CHECK_ARG(hq >= 1 && hkv >= 1 && hq % hkv == 0,
                 "n_query_heads=%d not divisible by n_kv_heads=%d", hq, hkv);
-  RCP_CHECK_ARG(hq / hkv <= kDecMaxGroup, "at most %d query heads per kv head", kDecMaxGroup);
   RCP_CHECK_ARG(batch >= 0 && max_kv_len >= 0 && kv_rows >= 0, "bad sizes");
   RCP_CHECK_ARG(kv_rows < INT32_MAX, "kv arena rows must fit int32");
   if (batch == 0) return RCP_OK;
@@ -659,7 +664,10 @@ static int decode_launch(const void* q, const void* k, const void* v, int64_t kv
                                   G::kSmemBytes));
     attr = true;
   }
-  dim3 grid(hkv, n_split, static_cast<unsigned>(batch));
+  const int n_hc = (hq / hkv + kDecMaxGroup - 1) / kDecMaxGroup;  // CTAs per KV head (16 query heads each)
+  RCP_CHECK_ARG(static_cast<int64_t>(hkv) * n_hc < (1ll << 31) && n_split < 65536 && batch < 65536,
+                "decode grid too large");
+  dim3 grid(static_cast<unsigned>(hkv * n_hc), n_split, static_cast<unsigned>(batch));
   decode_mma_kernel<kFp8><<<grid, kDecThreads, G::kSmemBytes, st>>>(prm);
   RCP_CUDA(cudaGetLastError());
   const int64_t rows = batch * hq;

@@ -91,7 +91,7 @@ def _decode_fp8(rc, q, kq, vq, ks, vs, starts, lens, hq, hkv):
 
 
 @pytest.mark.parametrize("hq,hkv,lens", [(128, 8, [5000, 70, 0, 1]), (32, 8, [4099, 64]), (16, 1, [20000]),
-                                         (8, 8, [63, 65, 129]), (64, 8, [100000])])
+                                         (8, 8, [63, 65, 129]), (64, 8, [100000]), (40, 1, [3000, 17])])
 def test_decode_fp8_kernel_vs_oracle(rc, hq, hkv, lens):
     """rcp_decode_attn_fp8: ragged lengths, empty segment, tail blocks, many
     splits, GQA groups 1..16; per-head scales spanning 400x."""

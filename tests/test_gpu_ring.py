@@ -184,7 +184,7 @@ def _bf16(x):
 
 
 @pytest.mark.parametrize("hq,hkv,lens", [(128, 8, [5000, 70, 0, 1]), (32, 8, [4099, 64]),
-                                         (16, 1, [20000])])
+                                         (16, 1, [20000]), (40, 1, [3000, 17]), (64, 2, [5000])])
 def test_decode_kernel_vs_oracle(rc, hq, hkv, lens):
     """rcp_decode_attn directly: one query per sequence against its cache
     segment (ragged lengths, empty segment, tail blocks, several splits)."""
