@@ -204,6 +204,77 @@ def workload_config(cfg, world: int, K: int) -> dict:
                 T // world * hq * D * 2 / 1e6, T // world * hkv * D * 2 / 1e6)}
 
 
+CFG1 = dict(T=4096, n=2, hq=8, hkv=1)  # BASELINE.json configs[0]: the reference's CPU-runnable case
+
+
+def _cfg1_inputs():
+    """cfg1 inputs: N(0,1) from default_rng(0), rounded to bf16."""
+    rng = np.random.default_rng(0)
+    T, hq, hkv = CFG1["T"], CFG1["hq"], CFG1["hkv"]
+    out = []
+    for h in (hq, hkv, hkv):
+        x = rng.standard_normal((T, h, D)).astype(np.float32)
+        u = x.view(np.uint32).astype(np.uint64)
+        out.append((((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16).astype(np.uint32).view(np.float32))
+    return out
+
+
+def cfg1_oracle_run() -> dict:
+    """The whole cfg1 workload (composed pass-KV, CP2 simulated ranks, T=4096,
+    8/1 heads) on the oracle port, one process, as the reference runs it."""
+    from oracle import ringcp_oracle as orc
+
+    q, k, v = _cfg1_inputs()
+    n = CFG1["n"]
+    t0 = time.perf_counter()
+    orc.ring_prefill([orc.Seq(0, 0, CFG1["T"])], [[0] * n], n, [orc.Cache(CFG1["hkv"], D) for _ in range(n)],
+                     [q], [k], [v], CFG1["hkv"])
+    sec = time.perf_counter() - t0
+    return {"seconds": sec, "cores": 1, "kind": "port",
+            "what": "cfg1: composed pass-KV, CP2 simulated ranks, T=4096, 8/1 heads, D=128 (whole workload)"}
+
+
+def cfg1_gpu_run(rc, dev) -> dict:
+    """cfg1 through this repo's simulated-rank ring (ring_pass_kv_prefill) on
+    one GPU: sharding, cache appends, 4 attention launches, merges."""
+    import torch
+
+    from paper_2411_01783_b200.kv_cache import RankKvCache
+    from paper_2411_01783_b200.ring import ring_pass_kv_prefill
+    from paper_2411_01783_b200.sharding import SequenceSpec, materialize_rank_block, plan_full_prefill
+
+    q, k, v = (torch.from_numpy(a).to(torch.bfloat16).to(dev) for a in _cfg1_inputs())
+    n = CFG1["n"]
+    plan = plan_full_prefill([SequenceSpec(0, 0, CFG1["T"])], n)
+    cfg = rc.GqaConfig(CFG1["hq"], CFG1["hkv"], D)
+    caches = [RankKvCache(CFG1["hkv"], D, capacity_tokens=8192, device=dev) for _ in range(n)]
+
+    def run():
+        for c in caches:
+            c.reset()
+        qb = [materialize_rank_block(plan, r, [q]) for r in range(n)]
+        kb = [materialize_rank_block(plan, r, [k]) for r in range(n)]
+        vb = [materialize_rank_block(plan, r, [v]) for r in range(n)]
+        return ring_pass_kv_prefill(plan, caches, qb, kb, vb, cfg)
+
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(10):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        run()
+        e.record()
+        torch.cuda.synchronize()
+        times.append(s.elapsed_time(e))
+    for c in caches:
+        c.close()
+    return {"ms": statistics.median(times),
+            "what": "cfg1: ring_pass_kv_prefill, CP2 simulated ranks on one GPU, T=4096, 8/1 heads "
+                    "(sharding + appends + 4 attention launches + merges; median of 10, CUDA events)"}
+
+
 def run_reference(args, cfg, rank, world):
     """--impl reference: the reference algorithm (oracle port; the reference is
     pure Python/numpy) on the host cores, rank 0 only."""
@@ -247,6 +318,8 @@ def run_reference(args, cfg, rank, world):
                          "sample": f"{cores} processes x {rows_per} query rows x {T} keys x "
                                    f"{len(range(0, hq, head_stride))} query heads per step"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        # BASELINE configs[0] run whole (not sampled) on the same host
+        "cfg1_full_run": None if args.no_cfg1 else cfg1_oracle_run(),
     }
     print(json.dumps(line), flush=True)
 
@@ -475,6 +548,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_port(T, hq, hkv, rows=args.cpu_rows)
+    cfg1 = cfg1_gpu_run(rc, dev) if (rank == 0 and not args.no_cfg1) else None
     value = flops_total / (ms * 1e-3) / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
@@ -493,6 +567,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "parity": parity,
         "e2e": e2e,
         "exposed_comm": exposed,
+        "cfg1": cfg1,
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
@@ -515,6 +590,8 @@ def main():
     ap.add_argument("--e2e-ranges", type=int, default=None,
                     help="query ranges per request in the e2e loop (default: the library's, one per 8192 slots, <= 16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cfg1", action="store_true",
+                    help="skip the whole-cfg1 timing (BASELINE configs[0]: GPU arm ~1 s, reference arm ~20 s)")
     ap.add_argument("--cpu-rows", type=int, default=8)
     ap.add_argument("--check", action="store_true",
                     help="after timing, check sampled rows of the last timed output against the fp64 oracle")
