@@ -163,7 +163,7 @@ inline int attn_v_box_rows(int version) { return attn_key_rows(version); }
 #define RCP_DEFAULT_ATTN_VERSION 4
 #endif
 constexpr int kDefaultAttnVersion = RCP_DEFAULT_ATTN_VERSION;
-int attn_n128_launch(const AttnParams& prm, int64_t grid, cudaStream_t st, bool turn);
+int attn_n128_launch(const AttnParams& prm, int64_t grid, cudaStream_t st, int form);
 int attn_pair_launch(const AttnParams& prm, int64_t n_pairs_heads, cudaStream_t st, bool col_split);
 
 }  // namespace rcp

@@ -599,7 +599,7 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
   if (version < 0) {
     const char* e = getenv("RCP_ATTN_VERSION");
     const int v = e ? atoi(e) : kDefaultAttnVersion;
-    version = (v == 4 || (v >= 12 && v <= 16)) ? v : kDefaultAttnVersion;
+    version = (v == 4 || (v >= 12 && v <= 17)) ? v : kDefaultAttnVersion;
   }
   const int krows = attn_key_rows(version);
   AttnParams prm;
@@ -658,8 +658,8 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
   RCP_CHECK_ARG(grid < (1ll << 30), "grid too large");
   if (version == 13 || version == 14) {
     if ((rc = attn_pair_launch(prm, grid, st, version == 14)) != RCP_OK) return rc;
-  } else if (version == 12 || version == 16) {
-    if ((rc = attn_n128_launch(prm, grid, st, version == 16)) != RCP_OK) return rc;
+  } else if (version == 12 || version == 16 || version == 17) {
+    if ((rc = attn_n128_launch(prm, grid, st, version == 16 ? 1 : version == 17 ? 2 : 0)) != RCP_OK) return rc;
   } else {
     static bool attr_set = false;
     if (!attr_set) {

@@ -64,7 +64,11 @@ constexpr int kPolyPairsN = RCP_POLY_PAIRS_N;
 // block j+1, ...; two named barriers per SMSP pair), so the MUFU / FMA pipes
 // serve one warp at a time and the tiles settle half a period apart — one
 // tile's exps run while the other tile's PV and next S occupy the tensor cores.
-template <bool kTurn>
+// kSplit (v17, RCP_ATTN_VERSION=17; FA4's split P arrive): the softmax
+// signals P in two parts — keys 0-95 once they are stored, keys 96-127 at the
+// end — and the issuer starts PV on the first part, so the tensor cores run
+// under the tail of the exps; the row sum moves after the final arrive.
+template <bool kTurn, bool kSplit>
 __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid_constant__ AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
@@ -73,7 +77,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid
   uint8_t* sKV = smem + 2 * kQTileBytes;  // kSlotsN K/V blocks
 
   __shared__ uint64_t bar_q, bar_full[kSlotsN], bar_empty[kSlotsN];
-  __shared__ uint64_t bar_s[2], bar_p[2], bar_o[2];
+  __shared__ uint64_t bar_s[2], bar_p[2], bar_o[2], bar_p2[2];
   __shared__ uint32_t tmem_slot;
 
   const int warp = static_cast<int>(warp_id());
@@ -95,6 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid
     for (int t = 0; t < 2; ++t) {
       mbar_init(&bar_s[t], 1);
       mbar_init(&bar_p[t], 128);
+      mbar_init(&bar_p2[t], 128);
       mbar_init(&bar_o[t], 1);
     }
     fence_mbar_init();
@@ -164,10 +169,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid
           mma_ss_lo(s_t, q_lo + (((kk >> 2) * kQBoxBytes + (kk & 3) * 32) >> 4),
                     ka + (((kk >> 2) * kKVBoxBytesN + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
       };
-      auto issue_pv = [&](uint32_t ld, bool acc) {
+      auto issue_pv = [&](uint32_t ld, bool acc, int kk0, int kk1) {
         const uint32_t va = v_lo + (((ld % kSlotsN) * kKVBytesN) >> 4);
 #pragma unroll
-        for (int kk = 0; kk < kKRowsN / 16; ++kk)
+        for (int kk = kk0; kk < kk1; ++kk)
           mma_ts_lo(o_t, s_t + kk * 8, va + ((kk * 2048) >> 4), idesc_o, (acc || kk > 0) ? 1u : 0u);
       };
       mbar_wait(&bar_q, 0);
@@ -181,7 +186,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid
         wait_load(ldv);
         mbar_wait(&bar_p[tt], it & 1);
         tc_fence_after();
-        issue_pv(ldv, it > 0);
+        if constexpr (kSplit) {
+          issue_pv(ldv, it > 0, 0, 6);  // keys 0-95 of P are stored
+          mbar_wait(&bar_p2[tt], it & 1);
+          tc_fence_after();
+          issue_pv(ldv, it > 0, 6, 8);
+        } else {
+          issue_pv(ldv, it > 0, 0, 8);
+        }
         TRACE(tt, it);
         if (last) mma_commit(&bar_o[tt]);
         mma_commit(&bar_empty[ldv % kSlotsN]);
@@ -336,10 +348,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid
                 p0 = ex2_approx(x.x);
                 p1 = ex2_approx(x.y);
               }
-              acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
+              if constexpr (kSplit) {
+                s[2 * ip] = p0;  // summed after P is handed over
+                s[2 * ip + 1] = p1;
+              } else {
+                acc2[i & 3] = fadd2(acc2[i & 3], f2(p0, p1));
+              }
               pk[i] = pack_bf16x2(p0, p1);
             }
             tmem_st16(s_addr + 16 * q, pk);
+            if constexpr (kSplit) {
+              if (q == 2) {  // keys 0-95 stored: PV may start on them
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(&bar_p[w]);
+              }
+            }
           }
         };
         turn_begin(it);
@@ -351,6 +375,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid
         }
         turn_end();
         if (t == 0 && w == 0) TRACE(10, it);
+        if constexpr (kSplit) {
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&bar_p2[w]);
+#pragma unroll
+          for (int i = 0; i < 64; ++i) acc2[i & 3] = fadd2(acc2[i & 3], f2(s[2 * i], s[2 * i + 1]));
+        }
         const float2 a01 = unf2(fadd2(acc2[0], acc2[1]));
         const float2 a23 = unf2(fadd2(acc2[2], acc2[3]));
         const float sum = (a01.x + a01.y) + (a23.x + a23.y);
@@ -363,10 +394,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid
         for (int i = 0; i < 32; ++i) pk[i] = 0u;
         tmem_st32(s_addr, pk);
         tmem_st32(s_addr + 32, pk);
+        if constexpr (kSplit) {
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&bar_p[w]);
+          mbar_arrive(&bar_p2[w]);
+        }
       }
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(&bar_p[w]);
+      if constexpr (!kSplit) {
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&bar_p[w]);
+      }
       if (t == 0) TRACE(3 + 2 * w, it);
     }
 
@@ -424,19 +463,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_n128_kernel(const __grid
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-int attn_n128_launch(const AttnParams& prm, int64_t grid, cudaStream_t st, bool turn) {
+int attn_n128_launch(const AttnParams& prm, int64_t grid, cudaStream_t st, int form) {
+  // form 0: v12, 1: v16 (exp turn-taking), 2: v17 (split P arrive)
   static bool attr_set = false;
   if (!attr_set) {
-    RCP_CUDA(cudaFuncSetAttribute(attn_fwd_n128_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemBytesN));
-    RCP_CUDA(cudaFuncSetAttribute(attn_fwd_n128_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemBytesN));
+    RCP_CUDA(cudaFuncSetAttribute(attn_fwd_n128_kernel<false, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytesN));
+    RCP_CUDA(cudaFuncSetAttribute(attn_fwd_n128_kernel<true, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytesN));
+    RCP_CUDA(cudaFuncSetAttribute(attn_fwd_n128_kernel<false, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytesN));
     attr_set = true;
   }
-  if (turn)
-    attn_fwd_n128_kernel<true><<<static_cast<unsigned>(grid), kThreads, kSmemBytesN, st>>>(prm);
+  const unsigned g = static_cast<unsigned>(grid);
+  if (form == 1)
+    attn_fwd_n128_kernel<true, false><<<g, kThreads, kSmemBytesN, st>>>(prm);
+  else if (form == 2)
+    attn_fwd_n128_kernel<false, true><<<g, kThreads, kSmemBytesN, st>>>(prm);
   else
-    attn_fwd_n128_kernel<false><<<static_cast<unsigned>(grid), kThreads, kSmemBytesN, st>>>(prm);
+    attn_fwd_n128_kernel<false, false><<<g, kThreads, kSmemBytesN, st>>>(prm);
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
 }
