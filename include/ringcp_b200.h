@@ -47,6 +47,10 @@ extern "C" {
 
 const char* rcp_last_error(void);
 const char* rcp_version(void);
+/* The attention kernel form this library runs: 4 (the product kernel); the
+ * A/B build (_ringcp_b200_ab.so) also carries the measured alternatives
+ * 12-17, selected by the RCP_ATTN_VERSION environment variable. */
+int rcp_attn_version(void);
 
 /* Workspace bytes rcp_attn_fwd needs for a (Tq, Tk) call (tile summaries). */
 size_t rcp_attn_workspace_bytes(int64_t tq, int64_t tk);

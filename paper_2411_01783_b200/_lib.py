@@ -63,6 +63,7 @@ SIGNATURES = {
         ctypes.POINTER(_c_void_p), _c_void_p, ctypes.POINTER(_i64), _i32, _i32, _i32, _i64, _c_void_p]),
     "rcp_fold_meta": (ctypes.c_int, [
         _c_void_p, _c_void_p, _c_void_p, _i64, _i32, _c_void_p, _c_void_p, _c_void_p]),
+    "rcp_attn_version": (_i32, []),
     "rcp_decode_workspace_bytes": (_size_t, [_i64, _i32, _i64]),
     "rcp_decode_attn": (ctypes.c_int, [
         _c_void_p, _c_void_p, _c_void_p, _i64, _i64, _c_void_p, _c_void_p, _i64, _i64,

@@ -163,6 +163,9 @@ inline int attn_v_box_rows(int version) { return attn_key_rows(version); }
 #define RCP_DEFAULT_ATTN_VERSION 4
 #endif
 constexpr int kDefaultAttnVersion = RCP_DEFAULT_ATTN_VERSION;
+#ifndef RCP_AB_FORMS
+#define RCP_AB_FORMS 0  // 1: the A/B build with the alternative kernel forms (v12-v17)
+#endif
 int attn_n128_launch(const AttnParams& prm, int64_t grid, cudaStream_t st, int form);
 int attn_pair_launch(const AttnParams& prm, int64_t n_pairs_heads, cudaStream_t st, bool col_split);
 

@@ -487,6 +487,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 }
 
 // ------------------------------------------------------------------ host side
+// Kernel form.  The product library has one: v4 (64-key blocks, this file).
+// The A/B build (-DRCP_AB_FORMS=1, _ringcp_b200_ab.so, with attn_fwd_n128.cu
+// and attn_fwd_pair.cu) also carries the measured alternatives v12-v17,
+// selected by RCP_ATTN_VERSION (read once); DESIGN.md §3 has their A/B.
+static int attn_version() {
+#if RCP_AB_FORMS
+  static int version = -1;
+  if (version < 0) {
+    const char* e = getenv("RCP_ATTN_VERSION");
+    const int v = e ? atoi(e) : kDefaultAttnVersion;
+    version = (v == 4 || (v >= 12 && v <= 17)) ? v : kDefaultAttnVersion;
+  }
+  return version;
+#else
+  return kDefaultAttnVersion;
+#endif
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -593,14 +611,7 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
                 "workspace too small: need %zu bytes", need);
   RCP_CHECK_ARG((reinterpret_cast<uintptr_t>(workspace) & 31) == 0, "workspace must be 32-byte aligned");
 
-  // Kernel form: v12 (128-key blocks, attn_fwd_n128.cu) or v4 (64-key
-  // blocks, this file); RCP_ATTN_VERSION selects one for A/B measurements.
-  static int version = -1;
-  if (version < 0) {
-    const char* e = getenv("RCP_ATTN_VERSION");
-    const int v = e ? atoi(e) : kDefaultAttnVersion;
-    version = (v == 4 || (v >= 12 && v <= 17)) ? v : kDefaultAttnVersion;
-  }
+  const int version = attn_version();
   const int krows = attn_key_rows(version);
   AttnParams prm;
   memset(&prm, 0, sizeof(prm));
@@ -656,24 +667,36 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
 
   const int64_t grid = static_cast<int64_t>(prm.n_qblk) * hq;
   RCP_CHECK_ARG(grid < (1ll << 30), "grid too large");
+#if RCP_AB_FORMS
   if (version == 13 || version == 14) {
     if ((rc = attn_pair_launch(prm, grid, st, version == 14)) != RCP_OK) return rc;
-  } else if (version == 12 || version == 16 || version == 17) {
+    return RCP_OK;
+  }
+  if (version == 12 || version == 16 || version == 17) {
     if ((rc = attn_n128_launch(prm, grid, st, version == 16 ? 1 : version == 17 ? 2 : 0)) != RCP_OK) return rc;
-  } else {
-    static bool attr_set = false;
-    if (!attr_set) {
-      RCP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kSmemBytes));
+    return RCP_OK;
+  }
+  if (version == 15) {
+    static bool attr15 = false;
+    if (!attr15) {
       RCP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     kSmemBytes));
-      attr_set = true;
+      attr15 = true;
     }
-    if (version == 15)
-      attn_fwd_kernel<1><<<static_cast<unsigned>(grid), kThreads, kSmemBytes, st>>>(prm);
-    else
-      attn_fwd_kernel<0><<<static_cast<unsigned>(grid), kThreads, kSmemBytes, st>>>(prm);
+    attn_fwd_kernel<1><<<static_cast<unsigned>(grid), kThreads, kSmemBytes, st>>>(prm);
+    RCP_CUDA(cudaGetLastError());
+    return RCP_OK;
   }
+#endif
+  static bool attr_set = false;
+  if (!attr_set) {
+    RCP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemBytes));
+    attr_set = true;
+  }
+  attn_fwd_kernel<0><<<static_cast<unsigned>(grid), kThreads, kSmemBytes, st>>>(prm);
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
 }
+
+extern "C" int rcp_attn_version(void) { return rcp::attn_version(); }

@@ -13,6 +13,7 @@ from paper_2411_01783_b200 import _lib  # noqa: E402
 from paper_2411_01783_b200.attention import attend_into  # noqa: E402
 from tests.test_gpu_attention_soak import _block, _reference, PAD_Q, PAD_K, POS_PAD_K  # noqa: E402
 
+assert _lib.load().rcp_attn_version() == int(os.environ["RCP_ATTN_VERSION"]), "kernel form not selected"
 worst_o, worst_l = 0.0, 0.0
 for case in range(8):
     rng = np.random.default_rng(500 + case)
