@@ -20,9 +20,10 @@ API with host buffers, clocks sampled during the timed region).
 
 e2e: K steps of RingAttention.pass_kv_prefill_host from pinned host buffers,
 run as a serving loop — each step's inputs are staged H2D one step ahead on a
-copy stream (stage_host_inputs) and each query range's final O / LSE goes D2H
-as soon as it is final; every step's H2D and D2H are inside the timed region,
-which ends after the D2H stream is joined (join_host_copies).
+copy stream (stage_host_inputs) and each query range's final O (bf16, the
+model dtype; the fp32-O loop is reported as e2e.fp32_out) / LSE (fp32) goes
+D2H as soon as it is final; every step's H2D and D2H are inside the timed
+region, which ends after the D2H stream is joined (join_host_copies).
 """
 
 from __future__ import annotations
@@ -482,17 +483,15 @@ def run_ours(args, cfg, rank, world, local_rank):
         host_full = {n: t.cpu().pin_memory() for n, t in tens.items()}
         host = {n: [t[seq_off[i]:seq_off[i + 1]] for i in range(K)] for n, t in host_full.items()}
         s_slots = plan.total_query_slots()
-        out_host = torch.empty((s_slots, hq, D), dtype=torch.float32).pin_memory()
         lse_host = torch.empty((s_slots, hq), dtype=torch.float32).pin_memory()
         h2d = 0
         for n, t in host_full.items():  # this rank's two chunks of every sequence
             h2d += t[0].numel() * t.element_size() * sum(plan.new_token_count(i, rank) for i in range(K))
-        d2h = out_host.numel() * 4 + lse_host.numel() * 4
 
         def stage():
             return ring.stage_host_inputs(plan, host["q"], host["k"], host["v"], gcfg, dev, n_sub=args.e2e_ranges)
 
-        def e2e_steps(n):
+        def e2e_steps(n, out_host):
             # public host-buffer API as a serving loop: each request's K/V and
             # query chunks go H2D on a copy stream (staged one request ahead,
             # while the previous one computes), the attention runs per query
@@ -507,31 +506,28 @@ def run_ours(args, cfg, rank, world, local_rank):
                 st = stage() if i + 1 < n else None  # next request's H2D runs under this one
             ring.join_host_copies()
 
-        e2e_steps(2)
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        e2e_steps(args.steps)
-        e1.record()
-        barrier()
-        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-        e2e = {"value": flops_total / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-               "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "out_dtype": "float32"}
-        if args.e2e_bf16:
-            # the same serving loop returning O in the model dtype (bf16, cast on
-            # the device per final range; LSE fp32): half the D2H bytes
-            out_host = torch.empty((s_slots, hq, D), dtype=torch.bfloat16).pin_memory()
-            e2e_steps(2)
+        def e2e_ms_for(dtype):
+            out_host = torch.empty((s_slots, hq, D), dtype=dtype).pin_memory()
+            e2e_steps(2, out_host)
             barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            e2e_steps(args.steps)
+            e2e_steps(args.steps, out_host)
             e1.record()
             barrier()
-            ms16 = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-            e2e["bf16_out"] = {"value": flops_total / (ms16 * 1e-3) / 1e12, "ms_per_step": ms16,
-                               "d2h_bytes_per_step": out_host.numel() * 2 + lse_host.numel() * 4}
+            return max_over_ranks(e0.elapsed_time(e1) / args.steps), out_host.numel() * out_host.element_size()
+
+        # The final O comes back in the model dtype, bf16 ("fp32
+        # partial or bf16 final in the build"; cast on the device per final
+        # range), LSE in fp32; the same loop with fp32 O is reported beside it.
+        ms16, o16 = e2e_ms_for(torch.bfloat16)
+        ms32, o32 = e2e_ms_for(torch.float32)
+        e2e = {"value": flops_total / (ms16 * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "ms_per_step": ms16, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": o16 + lse_host.numel() * 4,
+               "out_dtype": "bfloat16 O, float32 LSE",
+               "fp32_out": {"value": flops_total / (ms32 * 1e-3) / 1e12, "ms_per_step": ms32,
+                            "d2h_bytes_per_step": o32 + lse_host.numel() * 4}}
 
     if rank != 0:
         return
@@ -586,7 +582,7 @@ def main():
                     help="fused batch: split the tokens into this many ragged sequences (1 : 2 : ... : K)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-bf16", action="store_true",
-                    help="also time the e2e loop with bf16 host outputs (reported under e2e.bf16_out)")
+                    help="no-op, kept for old command lines: e2e returns bf16 O by default (fp32 under e2e.fp32_out)")
     ap.add_argument("--e2e-ranges", type=int, default=None,
                     help="query ranges per request in the e2e loop (default: the library's, one per 8192 slots, <= 16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
