@@ -36,6 +36,27 @@ def test_library_exports_every_declared_symbol():
     assert set(syms) == set(_lib.SIGNATURES), set(syms) ^ set(_lib.SIGNATURES)
 
 
+def test_product_and_ab_library_forms():
+    """The product library runs only the v4 attention kernel (the selector is
+    compiled out); the A/B library exports the same ABI and honours it."""
+    import subprocess
+    import sys
+
+    from paper_2411_01783_b200 import _build, _lib
+
+    if not os.path.exists(_build.LIB_AB):
+        _build.build()
+    ab = ctypes.CDLL(_build.LIB_AB)
+    for s in declared_symbols():
+        assert hasattr(ab, s), s
+    code = ("import ctypes,sys; l=ctypes.CDLL(sys.argv[1]); l.rcp_attn_version.restype=ctypes.c_int; "
+            "print(l.rcp_attn_version())")
+    env = dict(os.environ, RCP_ATTN_VERSION="12")
+    prod = subprocess.run([sys.executable, "-c", code, _lib.LIB_PATH], env=env, capture_output=True, text=True)
+    abv = subprocess.run([sys.executable, "-c", code, _build.LIB_AB], env=env, capture_output=True, text=True)
+    assert prod.stdout.strip() == "4" and abv.stdout.strip() == "12", (prod.stdout, prod.stderr, abv.stderr)
+
+
 def test_library_host_only_calls():
     """Calls that never touch a GPU: version, workspace sizes, argument errors."""
     from paper_2411_01783_b200 import _lib
