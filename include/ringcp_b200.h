@@ -143,8 +143,9 @@ int rcp_decode_attn_fp8(const void* q, const void* k, const void* v, int64_t kv_
 
 /* bf16 rows -> e4m3 rows: row j of src ([n_rows, hkv * head_dim], row stride
  * in elements) is written to dst row dst_rows[j] (device int64; NULL = row j),
- * each element satfinite_rn(x / scale[head]) with an IEEE fp32 division
- * (bit-exact with oracle/ringcp_oracle.py::quantize_e4m3). */
+ * each element satfinite_rn(x * (1 / scale[head])) in IEEE fp32 (the
+ * reciprocal once per head; bit-exact with
+ * oracle/ringcp_oracle.py::quantize_e4m3). */
 int rcp_kv_quantize_e4m3(void* dst, int64_t dst_row_stride, const int64_t* dst_rows, const void* src,
                          int64_t src_row_stride, int64_t n_rows, int32_t hkv, int32_t head_dim,
                          const float* scale, void* stream);

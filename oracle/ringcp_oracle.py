@@ -585,11 +585,12 @@ def e4m3_scale(rows, n_kv_heads: int) -> np.ndarray:
 
 
 def quantize_e4m3(rows, scale) -> np.ndarray:
-    """rows [n, H, D] (float32 / bf16 values) -> e4m3 bytes: RNE(x / scale[h])
-    with the division in IEEE float32 (rcp_kv_quantize_e4m3)."""
+    """rows [n, H, D] (float32 / bf16 values) -> e4m3 bytes: RNE(x * inv[h])
+    with inv = 1 / scale[h] and the product in IEEE float32
+    (rcp_kv_quantize_e4m3)."""
     r = np.asarray(rows, np.float32)
-    s = np.asarray(scale, np.float32).reshape(1, -1, 1)
-    return e4m3_encode((r / s).astype(np.float32))
+    inv = (np.float32(1.0) / np.asarray(scale, np.float32)).astype(np.float32).reshape(1, -1, 1)
+    return e4m3_encode((r * inv).astype(np.float32))
 
 
 def dequantize_e4m3(bits, scale) -> np.ndarray:

@@ -679,58 +679,73 @@ static int decode_launch(const void* q, const void* k, const void* v, int64_t kv
 
 // ---------------------------------------------------------------- e4m3 KV rows
 // Row j of src (bf16 [n_rows, hkv*head_dim], row stride in elements) ->
-// dst row (dst_rows ? dst_rows[j] : j): e4m3 = satfinite_rn(x / scale[head]),
-// the division IEEE round-to-nearest (the oracle's fp32 division bit for bit).
-// One thread per 8 elements: a 16-byte load and an 8-byte store.
-__global__ void kv_quantize_kernel(uint8_t* __restrict__ dst, int64_t dst_stride, const int64_t* __restrict__ dst_rows,
-                                   const __nv_bfloat16* __restrict__ src, int64_t src_stride, int64_t n_rows,
-                                   int row_elems, int head_dim, const float* __restrict__ scale) {
-  const int per_row = row_elems >> 3;
-  const int64_t n = n_rows * per_row;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t j = i / per_row;
-    const int c = static_cast<int>(i - j * per_row) << 3;
-    const float s = __ldg(scale + c / head_dim);
-    const uint4 x = __ldg(reinterpret_cast<const uint4*>(src + j * src_stride + c));
-    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-    uint16_t e[4];
+// dst row (dst_rows ? dst_rows[j] : j): e4m3 = satfinite_rn(x * inv[head]) with
+// inv = 1 / scale (IEEE fp32 division, once per head) and an fp32 multiply —
+// bit for bit oracle/ringcp_oracle.py::quantize_e4m3.  One warp per row at a
+// time, each lane 8 elements (a 16-byte load, an 8-byte store) per step; the
+// per-head factors sit in shared memory (hkv <= 1024).
+constexpr int kKvRowThreads = 256;
+__global__ void __launch_bounds__(kKvRowThreads) kv_quantize_kernel(
+    uint8_t* __restrict__ dst, int64_t dst_stride, const int64_t* __restrict__ dst_rows,
+    const __nv_bfloat16* __restrict__ src, int64_t src_stride, int64_t n_rows, int hkv, int hd_chunks,
+    const float* __restrict__ scale) {
+  __shared__ float s_inv[1024];
+  for (int h = threadIdx.x; h < hkv; h += blockDim.x) s_inv[h] = __fdiv_rn(1.0f, __ldg(scale + h));
+  __syncthreads();
+  const int per_row = hkv * hd_chunks;  // 8-element chunks per row
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); j < n_rows; j += warps) {
+    const __nv_bfloat16* srow = src + j * src_stride;
+    uint8_t* drow = dst + (dst_rows ? __ldg(dst_rows + j) : j) * dst_stride;
+#pragma unroll 4
+    for (int c = lane; c < per_row; c += 32) {
+      const float inv = s_inv[c / hd_chunks];
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(srow) + c);
+      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+      uint16_t e[4];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[t]));
-      const float lo = __fdiv_rn(f.x, s), hi = __fdiv_rn(f.y, s);
-      asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(e[t]) : "f"(hi), "f"(lo));
+      for (int t = 0; t < 4; ++t) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[t]));
+        const float lo = __fmul_rn(f.x, inv), hi = __fmul_rn(f.y, inv);
+        asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(e[t]) : "f"(hi), "f"(lo));
+      }
+      uint2 out;
+      out.x = static_cast<uint32_t>(e[0]) | (static_cast<uint32_t>(e[1]) << 16);
+      out.y = static_cast<uint32_t>(e[2]) | (static_cast<uint32_t>(e[3]) << 16);
+      reinterpret_cast<uint2*>(drow)[c] = out;
     }
-    const int64_t row = dst_rows ? __ldg(dst_rows + j) : j;
-    uint2 out;
-    out.x = static_cast<uint32_t>(e[0]) | (static_cast<uint32_t>(e[1]) << 16);
-    out.y = static_cast<uint32_t>(e[2]) | (static_cast<uint32_t>(e[3]) << 16);
-    *reinterpret_cast<uint2*>(dst + row * dst_stride + c) = out;
   }
 }
 
-// x = e4m3 * scale[head] in fp32, rounded to bf16 (RN).
-__global__ void kv_dequantize_kernel(__nv_bfloat16* __restrict__ dst, int64_t dst_stride,
-                                     const uint8_t* __restrict__ src, int64_t src_stride, int64_t n_rows,
-                                     int row_elems, int head_dim, const float* __restrict__ scale) {
-  const int per_row = row_elems >> 3;
-  const int64_t n = n_rows * per_row;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t j = i / per_row;
-    const int c = static_cast<int>(i - j * per_row) << 3;
-    const float s = __ldg(scale + c / head_dim);
-    const uint2 x = __ldg(reinterpret_cast<const uint2*>(src + j * src_stride + c));
-    const uint32_t w[2] = {x.x, x.y};
-    uint32_t out[4];
+// x = e4m3 * scale[head] in fp32, rounded to bf16 (RN); same walk as above.
+__global__ void __launch_bounds__(kKvRowThreads) kv_dequantize_kernel(
+    __nv_bfloat16* __restrict__ dst, int64_t dst_stride, const uint8_t* __restrict__ src, int64_t src_stride,
+    int64_t n_rows, int hkv, int hd_chunks, const float* __restrict__ scale) {
+  __shared__ float s_sc[1024];
+  for (int h = threadIdx.x; h < hkv; h += blockDim.x) s_sc[h] = __ldg(scale + h);
+  __syncthreads();
+  const int per_row = hkv * hd_chunks;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); j < n_rows; j += warps) {
+    const uint8_t* srow = src + j * src_stride;
+    __nv_bfloat16* drow = dst + j * dst_stride;
+#pragma unroll 4
+    for (int c = lane; c < per_row; c += 32) {
+      const float sc = s_sc[c / hd_chunks];
+      const uint2 x = __ldg(reinterpret_cast<const uint2*>(srow) + c);
+      const uint32_t w[2] = {x.x, x.y};
+      uint32_t out[4];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const uint32_t h2 = e4m3x2_f16x2(w[t >> 1] >> (16 * (t & 1)));
-      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h2));
-      const __nv_bfloat162 b = __floats2bfloat162_rn(f.x * s, f.y * s);
-      out[t] = *reinterpret_cast<const uint32_t*>(&b);
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t h2 = e4m3x2_f16x2(w[t >> 1] >> (16 * (t & 1)));
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h2));
+        const __nv_bfloat162 bb = __floats2bfloat162_rn(__fmul_rn(f.x, sc), __fmul_rn(f.y, sc));
+        out[t] = *reinterpret_cast<const uint32_t*>(&bb);
+      }
+      reinterpret_cast<uint4*>(drow)[c] = make_uint4(out[0], out[1], out[2], out[3]);
     }
-    *reinterpret_cast<uint4*>(dst + j * dst_stride + c) = make_uint4(out[0], out[1], out[2], out[3]);
   }
 }
 
@@ -764,6 +779,11 @@ __global__ void kv_scale_kernel(unsigned* amax_bits, float* scale, int hkv) {
   if (h < hkv) scale[h] = __fdiv_rn(fmaxf(__uint_as_float(amax_bits[h]), 5.9604644775390625e-08f), 448.f);
 }
 
+// One warp per row per step: up to 16 resident 256-thread CTAs per SM worth of warps.
+static int kv_rows_grid(int64_t n_rows) {
+  const int64_t b = (n_rows + 7) / 8;
+  return static_cast<int>(b < 1 ? 1 : (b > 148 * 8 ? 148 * 8 : b));
+}
 static int rows_grid(int64_t items) {
   const int64_t b = (items + 255) / 256;
   return static_cast<int>(b < 1 ? 1 : (b > 148 * 16 ? 148 * 16 : b));
@@ -798,10 +818,10 @@ extern "C" int rcp_kv_quantize_e4m3(void* dst, int64_t dst_row_stride, const int
                     src_row_stride >= hkv * head_dim, "bad row stride");
   RCP_CHECK_ARG((reinterpret_cast<uintptr_t>(dst) & 7) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0,
                 "misaligned rows");
-  const int row_elems = hkv * head_dim;
-  kv_quantize_kernel<<<rows_grid(n_rows * (row_elems >> 3)), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  RCP_CHECK_ARG(hkv <= 1024, "at most 1024 kv heads");
+  kv_quantize_kernel<<<kv_rows_grid(n_rows), kKvRowThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<uint8_t*>(dst), dst_row_stride, dst_rows, static_cast<const __nv_bfloat16*>(src),
-      src_row_stride, n_rows, row_elems, head_dim, scale);
+      src_row_stride, n_rows, hkv, head_dim >> 3, scale);
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
 }
@@ -816,10 +836,10 @@ extern "C" int rcp_kv_dequantize_e4m3(void* dst, int64_t dst_row_stride, const v
                     src_row_stride >= hkv * head_dim, "bad row stride");
   RCP_CHECK_ARG((reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (reinterpret_cast<uintptr_t>(src) & 7) == 0,
                 "misaligned rows");
-  const int row_elems = hkv * head_dim;
-  kv_dequantize_kernel<<<rows_grid(n_rows * (row_elems >> 3)), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  RCP_CHECK_ARG(hkv <= 1024, "at most 1024 kv heads");
+  kv_dequantize_kernel<<<kv_rows_grid(n_rows), kKvRowThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<__nv_bfloat16*>(dst), dst_row_stride, static_cast<const uint8_t*>(src), src_row_stride, n_rows,
-      row_elems, head_dim, scale);
+      hkv, head_dim >> 3, scale);
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
 }

@@ -1,4 +1,5 @@
-"""Achieved HBM bandwidth of the byte-moving kernels (K0 shard gather, K2 merge).
+"""Achieved HBM bandwidth of the byte-moving kernels (K0 shard gather / scatter,
+K2 merge, the e4m3 KV quantise / dequantise rows).
 
   python tools/bench_hbm_kernels.py
 
@@ -68,6 +69,37 @@ def main():
     nbytes = 2 * slots * H * D * 2 + slots * 8
     out["K0_shard_gather"] = dict(shape=f"rank 3 of CP8, 1M tokens, [{slots},{H},{D}] bf16", ms=ms, bytes=nbytes,
                                   gbs=nbytes / ms / 1e6, frac=nbytes / ms / 1e6 / peak)
+    # K0 shard scatter (the inverse): the same rank block back to token order
+    from paper_2411_01783_b200.sharding import scatter_rank_block
+
+    blk = materialize_rank_block(plan, 3, [q]).data
+    dst = torch.empty_like(q)
+    ms = timed(lambda: scatter_rank_block(plan, 3, blk, [dst]))
+    valid = plan.new_token_count(0, 3)
+    nbytes = 2 * valid * H * D * 2
+    out["K0_shard_scatter"] = dict(shape=f"rank 3 of CP8, 1M tokens, {valid} valid slots x [{H},{D}] bf16", ms=ms,
+                                   bytes=nbytes, gbs=nbytes / ms / 1e6, frac=nbytes / ms / 1e6 / peak)
+    del q, blk, dst
+    torch.cuda.empty_cache()
+    # e4m3 KV rows: quantise (bf16 -> e4m3) and dequantise (e4m3 -> bf16), 1M rows x 8 heads x 128
+    from paper_2411_01783_b200 import _lib
+
+    lib = _lib.load()
+    R, HK = 1 << 20, 8
+    x = torch.randn(R, HK, D, device="cuda", dtype=torch.bfloat16)
+    e8 = torch.empty(R, HK, D, device="cuda", dtype=torch.uint8)
+    back = torch.empty_like(x)
+    sc = torch.full((HK,), 0.01, device="cuda")
+    row = HK * D
+    ms = timed(lambda: _lib.check(lib.rcp_kv_quantize_e4m3(e8.data_ptr(), row, 0, x.data_ptr(), row, R, HK, D,
+                                                           sc.data_ptr(), _lib.stream_handle())))
+    nbytes = R * row * 3
+    out["kv_quantize_e4m3"] = dict(shape=f"[{R},{HK},{D}] bf16 -> e4m3", ms=ms, bytes=nbytes,
+                                   gbs=nbytes / ms / 1e6, frac=nbytes / ms / 1e6 / peak)
+    ms = timed(lambda: _lib.check(lib.rcp_kv_dequantize_e4m3(back.data_ptr(), row, e8.data_ptr(), row, R, HK, D,
+                                                             sc.data_ptr(), _lib.stream_handle())))
+    out["kv_dequantize_e4m3"] = dict(shape=f"[{R},{HK},{D}] e4m3 -> bf16", ms=ms, bytes=nbytes,
+                                     gbs=nbytes / ms / 1e6, frac=nbytes / ms / 1e6 / peak)
     out["peak_gbs"] = peak
     print(json.dumps(out, indent=1))
 
