@@ -154,7 +154,8 @@ int rcp_kv_quantize_e4m3(void* dst, int64_t dst_row_stride, const int64_t* dst_r
 int rcp_kv_dequantize_e4m3(void* dst, int64_t dst_row_stride, const void* src, int64_t src_row_stride,
                            int64_t n_rows, int32_t hkv, int32_t head_dim, const float* scale, void* stream);
 /* Per-KV-head scale from bf16 rows: scale[h] = max(absmax_h, 2^-24) / 448
- * (fp32 IEEE division).  workspace: hkv * 4 bytes of device memory. */
+ * (fp32 IEEE division) rounded up to a power of two (then e4m3 * scale is
+ * exact in bf16: prefill and decode read the same values).  workspace: hkv * 4 bytes of device memory. */
 int rcp_kv_calibrate_e4m3(const void* src, int64_t src_row_stride, int64_t n_rows, int32_t hkv,
                           int32_t head_dim, float* scale, void* workspace, void* stream);
 

@@ -576,12 +576,23 @@ def e4m3_decode(b) -> np.ndarray:
     return np.where((b & 0x7F) == 0x7F, np.nan, s * val)
 
 
+def pow2_ceil_f32(v) -> np.ndarray:
+    """Smallest power of two >= v for positive normal float32 v (bit-exact:
+    round the exponent up unless the mantissa is zero)."""
+    u = np.asarray(v, np.float32).view(np.uint32).astype(np.uint64)
+    return ((u + 0x7FFFFF) & 0xFF800000).astype(np.uint32).view(np.float32)
+
+
 def e4m3_scale(rows, n_kv_heads: int) -> np.ndarray:
-    """Per-KV-head calibration scale max(absmax, 2^-24) / 448 in float32
-    (rcp_kv_calibrate_e4m3)."""
+    """Per-KV-head calibration scale (rcp_kv_calibrate_e4m3): max(absmax,
+    2^-24) / 448 in float32, rounded UP to a power of two.  A power-of-two
+    scale keeps the head's absmax within e4m3's range and makes e4m3 * scale
+    exactly representable in bf16, so the bf16 rows the prefill reads and the
+    scaled e4m3 the decode kernel reads are the same values."""
     r = np.asarray(rows, np.float32).reshape(-1, n_kv_heads, np.asarray(rows).shape[-1])
     amax = np.abs(r).max(axis=(0, 2)) if r.shape[0] else np.zeros(n_kv_heads, np.float32)
-    return (np.maximum(amax, np.float32(2.0 ** -24)).astype(np.float32) / np.float32(E4M3_MAX)).astype(np.float32)
+    v = (np.maximum(amax, np.float32(2.0 ** -24)).astype(np.float32) / np.float32(E4M3_MAX)).astype(np.float32)
+    return pow2_ceil_f32(v)
 
 
 def quantize_e4m3(rows, scale) -> np.ndarray:

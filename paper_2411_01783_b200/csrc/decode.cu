@@ -774,9 +774,15 @@ __global__ void kv_absmax_kernel(const __nv_bfloat16* __restrict__ src, int64_t 
   for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
   if ((threadIdx.x & 31) == 0) atomicMax(amax_bits + h, __float_as_uint(m));
 }
+// scale = max(amax, 2^-24) / 448 rounded UP to a power of two: the absmax stays
+// in range, and e4m3 * scale is exact in bf16, so the prefill's bf16 rows and
+// the decode kernel's scaled e4m3 are the same values.
 __global__ void kv_scale_kernel(unsigned* amax_bits, float* scale, int hkv) {
   const int h = threadIdx.x;
-  if (h < hkv) scale[h] = __fdiv_rn(fmaxf(__uint_as_float(amax_bits[h]), 5.9604644775390625e-08f), 448.f);
+  if (h < hkv) {
+    const float v = __fdiv_rn(fmaxf(__uint_as_float(amax_bits[h]), 5.9604644775390625e-08f), 448.f);
+    scale[h] = __uint_as_float((__float_as_uint(v) + 0x7FFFFFu) & 0xFF800000u);
+  }
 }
 
 // One warp per row per step: up to 16 resident 256-thread CTAs per SM worth of warps.

@@ -12,7 +12,8 @@ message builder need.
 FP8 KV (``kv_dtype="e4m3"``; beyond the SPEC's bf16
 contract): K/V rows are stored as OCP e4m3 bytes with one fp32 scale per KV
 head (value = scale * e4m3; scales given, or calibrated from the first append
-as absmax / 448).  Rows are quantised on the device as they are appended
+as absmax / 448 rounded up to a power of two, which makes e4m3 * scale exact
+in bf16).  Rows are quantised on the device as they are appended
 (rcp_kv_quantize_e4m3), decode reads them directly (rcp_decode_attn_fp8, half
 the bytes per key), and snapshots / prefill messages dequantise them to bf16
 (rcp_kv_dequantize_e4m3).  ``dtype`` stays the dtype rows are handed out in.
@@ -245,7 +246,8 @@ class RankKvCache:
         return torch.from_numpy(a).to(self.device)
 
     def _calibrate(self, k_rows: torch.Tensor, v_rows: torch.Tensor) -> None:
-        """Per-KV-head scales absmax / 448 from the first rows appended."""
+        """Per-KV-head scales (absmax / 448, rounded up to a power of two) from
+        the first rows appended."""
         lib = _lib.load()
         ws = torch.empty(self.n_kv_heads, dtype=torch.int32, device=self.device)
         for name, rows in (("k_scale", k_rows), ("v_scale", v_rows)):
