@@ -141,6 +141,19 @@ int rcp_decode_attn_fp8(const void* q, const void* k, const void* v, int64_t kv_
                         const float* k_scale, const float* v_scale, float* o, float* lse, void* workspace,
                         size_t workspace_bytes, void* stream);
 
+/* rcp_decode_attn / rcp_decode_attn_fp8 with the combined rows ROUTED: row
+ * block d of the batch (batch / n_dst queries each) goes to o_dst[d] / lse_dst[d]
+ * (DEVICE arrays of n_dst base pointers, e.g. the owners' CUDA-IPC receive
+ * buffers) at query row dst_row_offset + (b % (batch / n_dst)) — the All2All
+ * of Alg. 4 done by the combine kernel's own stores over NVLink.  k_scale /
+ * v_scale NULL selects bf16 K/V, non-NULL e4m3. */
+int rcp_decode_attn_routed(const void* q, const void* k, const void* v, int64_t kv_row_stride,
+                           int64_t kv_rows, const int64_t* kv_start, const int64_t* kv_len, int64_t batch,
+                           int64_t max_kv_len, int32_t hq, int32_t hkv, int32_t head_dim, float scale,
+                           const float* k_scale, const float* v_scale, float* const* o_dst,
+                           float* const* lse_dst, int32_t n_dst, int64_t dst_row_offset, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
 /* bf16 rows -> e4m3 rows: row j of src ([n_rows, hkv * head_dim], row stride
  * in elements) is written to dst row dst_rows[j] (device int64; NULL = row j),
  * each element satfinite_rn(x * (1 / scale[head])) in IEEE fp32 (the
@@ -163,6 +176,21 @@ int rcp_kv_calibrate_e4m3(const void* src, int64_t src_row_stride, int64_t n_row
  * attention output in the model dtype, so the host-buffer path copies half the
  * bytes back (RingAttention.pass_kv_prefill_host with bf16 host outputs). */
 int rcp_cast_f32_bf16(void* dst, const float* src, int64_t n, void* stream);
+
+/* Device-side transport over CUDA-IPC peer memory (the decode step's Q
+ * all-gather and partial All2All without NCCL, graph-capturable):
+ *   rcp_p2p_epoch_advance: *epoch += 1 (once per step, every rank);
+ *   rcp_p2p_put:    copy `bytes` (multiple of 16) of src to each of the n
+ *                   destinations dst[0..n) (DEVICE array of pointers);
+ *   rcp_p2p_signal: publish *epoch to each flag_dst[p] (DEVICE array; this
+ *                   rank's flag slot in peer p's buffer), release, system scope;
+ *   rcp_p2p_wait:   wait until flags[0..n) (this rank's own slots) all reach
+ *                   *epoch, acquire; after ~9 s sets *timed_out = 1 and returns
+ *                   (the caller checks it) instead of hanging. */
+int rcp_p2p_epoch_advance(uint64_t* epoch, void* stream);
+int rcp_p2p_put(void* const* dst, int32_t n, const void* src, size_t bytes, void* stream);
+int rcp_p2p_signal(uint64_t* const* flag_dst, int32_t n, const uint64_t* epoch, void* stream);
+int rcp_p2p_wait(const uint64_t* flags, int32_t n, const uint64_t* epoch, int32_t* timed_out, void* stream);
 
 /* Decode-graph helper: copy row *counter of the device int64 table
  * [n_rows, row_elems] to dst, then increment *counter (device int64, clamped

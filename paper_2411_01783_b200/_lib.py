@@ -71,6 +71,14 @@ SIGNATURES = {
     "rcp_decode_attn_fp8": (ctypes.c_int, [
         _c_void_p, _c_void_p, _c_void_p, _i64, _i64, _c_void_p, _c_void_p, _i64, _i64,
         _i32, _i32, _i32, _f32, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size_t, _c_void_p]),
+    "rcp_decode_attn_routed": (ctypes.c_int, [
+        _c_void_p, _c_void_p, _c_void_p, _i64, _i64, _c_void_p, _c_void_p, _i64, _i64,
+        _i32, _i32, _i32, _f32, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _i32, _i64, _c_void_p, _size_t,
+        _c_void_p]),
+    "rcp_p2p_epoch_advance": (ctypes.c_int, [_c_void_p, _c_void_p]),
+    "rcp_p2p_put": (ctypes.c_int, [_c_void_p, _i32, _c_void_p, _size_t, _c_void_p]),
+    "rcp_p2p_signal": (ctypes.c_int, [_c_void_p, _i32, _c_void_p, _c_void_p]),
+    "rcp_p2p_wait": (ctypes.c_int, [_c_void_p, _i32, _c_void_p, _c_void_p, _c_void_p]),
     "rcp_kv_quantize_e4m3": (ctypes.c_int, [
         _c_void_p, _i64, _c_void_p, _c_void_p, _i64, _i64, _i32, _i32, _c_void_p, _c_void_p]),
     "rcp_kv_dequantize_e4m3": (ctypes.c_int, [
@@ -84,7 +92,7 @@ _lib = None
 # Kernel launches issued through this binding (per C-ABI call: rcp_attn_fwd 4 =
 # two tile summaries + active lists + attention; rcp_decode_attn(_fp8) 2 =
 # split-KV + combine; rcp_kv_calibrate_e4m3 2 = absmax + scale; others 1).
-LAUNCHES_PER_CALL = {"rcp_attn_fwd": 4, "rcp_decode_attn": 2, "rcp_decode_attn_fp8": 2,
+LAUNCHES_PER_CALL = {"rcp_attn_fwd": 4, "rcp_decode_attn": 2, "rcp_decode_attn_fp8": 2, "rcp_decode_attn_routed": 2,
                      "rcp_kv_calibrate_e4m3": 2}
 launch_count = 0
 

@@ -326,6 +326,51 @@ static unsigned grid_for(int64_t work, int threads) {
   return static_cast<unsigned>(b);
 }
 
+// ------------------------------------------------- P2P (NVLink peer memory) transport
+// The decode step's Q all-gather and partial All2All as plain kernels over
+// CUDA-IPC-mapped buffers (rcp_ipc_*), graph-capturable: a put kernel stores
+// into every peer's buffer, a signal kernel publishes the step's epoch into
+// each peer's flag slot for this rank (release, system scope), and a wait
+// kernel spins until every peer's flag in this rank's buffer reached the
+// epoch (acquire).  The epoch is a device counter advanced once per step.
+__global__ void p2p_epoch_kernel(unsigned long long* epoch) { *epoch += 1ull; }
+
+__global__ void __launch_bounds__(256) p2p_put_kernel(void* const* __restrict__ dst, int n,
+                                                      const uint4* __restrict__ src, int64_t n16) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n16;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint4 v = __ldg(src + i);
+    for (int p = 0; p < n; ++p) reinterpret_cast<uint4*>(dst[p])[i] = v;
+  }
+  __threadfence_system();
+}
+
+__global__ void p2p_signal_kernel(unsigned long long* const* __restrict__ flag_dst, int n,
+                                  const unsigned long long* __restrict__ epoch) {
+  __threadfence_system();
+  const unsigned long long e = *epoch;
+  for (int p = threadIdx.x; p < n; p += blockDim.x)
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag_dst[p]), "l"(e) : "memory");
+}
+
+__global__ void p2p_wait_kernel(const unsigned long long* __restrict__ flags, int n,
+                                const unsigned long long* __restrict__ epoch, int* __restrict__ timed_out) {
+  const unsigned long long e = *epoch;
+  const long long t0 = clock64();
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    unsigned long long v;
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + p) : "memory");
+      if (v >= e) break;
+      if (clock64() - t0 > (1ll << 34)) {  // ~9 s: a peer is gone; report instead of hanging
+        atomicExch(timed_out, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+}
+
 }  // namespace rcp
 
 using namespace rcp;
@@ -484,6 +529,42 @@ int rcp_cast_f32_bf16(void* dst, const float* src, int64_t n, void* stream) {
                 "src must be 16-byte and dst 8-byte aligned");
   cast_f32_bf16_kernel<<<grid_for(n / 4, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const float4*>(src), static_cast<uint2*>(dst), n / 4);
+  RCP_CUDA(cudaGetLastError());
+  return RCP_OK;
+}
+
+int rcp_p2p_epoch_advance(uint64_t* epoch, void* stream) {
+  RCP_CHECK_ARG(epoch, "null epoch");
+  p2p_epoch_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<unsigned long long*>(epoch));
+  RCP_CUDA(cudaGetLastError());
+  return RCP_OK;
+}
+
+int rcp_p2p_put(void* const* dst, int32_t n, const void* src, size_t bytes, void* stream) {
+  RCP_CHECK_ARG(dst && src && n >= 1 && bytes % 16 == 0, "bad p2p put (bytes %% 16 == 0, n >= 1)");
+  RCP_CHECK_ARG((reinterpret_cast<uintptr_t>(src) & 15) == 0, "src must be 16-byte aligned");
+  const int64_t n16 = static_cast<int64_t>(bytes / 16);
+  if (n16 == 0) return RCP_OK;
+  const int64_t blocks = (n16 + 255) / 256;
+  p2p_put_kernel<<<static_cast<unsigned>(blocks < 296 ? blocks : 296), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      dst, n, static_cast<const uint4*>(src), n16);
+  RCP_CUDA(cudaGetLastError());
+  return RCP_OK;
+}
+
+int rcp_p2p_signal(uint64_t* const* flag_dst, int32_t n, const uint64_t* epoch, void* stream) {
+  RCP_CHECK_ARG(flag_dst && epoch && n >= 1, "bad p2p signal");
+  p2p_signal_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<unsigned long long* const*>(flag_dst), n, reinterpret_cast<const unsigned long long*>(epoch));
+  RCP_CUDA(cudaGetLastError());
+  return RCP_OK;
+}
+
+int rcp_p2p_wait(const uint64_t* flags, int32_t n, const uint64_t* epoch, int32_t* timed_out, void* stream) {
+  RCP_CHECK_ARG(flags && epoch && timed_out && n >= 1, "bad p2p wait");
+  p2p_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const unsigned long long*>(flags), n, reinterpret_cast<const unsigned long long*>(epoch),
+      timed_out);
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
 }

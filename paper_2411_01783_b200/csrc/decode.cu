@@ -445,9 +445,19 @@ __global__ void __launch_bounds__(kDecThreads) decode_mma_kernel(const __grid_co
 // warp 0 folds the 8 warp partials in warp order.  Deterministic; the same
 // kernel serves every decode transport, so they stay bit-identical.
 constexpr int kCombineWarps = 8;
+// Output routing (rcp_decode_attn_routed): with o_dst non-null, row r goes to
+// destination d = r / rows_per_dst (a DEVICE array of base pointers, e.g. the
+// owners' peer-mapped receive buffers), row dst_row_offset + r % rows_per_dst.
+struct CombineRoute {
+  float* const* o_dst;
+  float* const* lse_dst;
+  int64_t rows_per_dst;
+  int64_t dst_row_offset;
+};
+
 __global__ void __launch_bounds__(kCombineWarps * 32) decode_combine_kernel(
     const float* __restrict__ part_o, const float* __restrict__ part_lse, int64_t rows, int n_split,
-    float* __restrict__ o, float* __restrict__ lse) {
+    float* __restrict__ o, float* __restrict__ lse, CombineRoute route) {
   __shared__ float4 s_acc[kCombineWarps][32];
   __shared__ float s_m[kCombineWarps], s_l[kCombineWarps];
   const int64_t row = blockIdx.x;
@@ -497,8 +507,16 @@ __global__ void __launch_bounds__(kCombineWarps * 32) decode_combine_kernel(
   }
   const bool has = lt > 0.f;
   const float inv = has ? 1.0f / lt : 0.f;
-  reinterpret_cast<float4*>(o + row * 128)[lane] = make_float4(r.x * inv, r.y * inv, r.z * inv, r.w * inv);
-  if (lane == 0) lse[row] = has ? mt + logf(lt) : -INFINITY;
+  float* orow = o + row * 128;
+  float* lrow = lse + row;
+  if (route.o_dst) {  // e.g. straight into the owner's receive buffer over NVLink
+    const int64_t d = row / route.rows_per_dst, rr = route.dst_row_offset + row % route.rows_per_dst;
+    orow = route.o_dst[d] + rr * 128;
+    lrow = route.lse_dst[d] + rr;
+  }
+  reinterpret_cast<float4*>(orow)[lane] = make_float4(r.x * inv, r.y * inv, r.z * inv, r.w * inv);
+  if (lane == 0) *lrow = has ? mt + logf(lt) : -INFINITY;
+  if (route.o_dst) __threadfence_system();  // peer stores visible before the step's signal
 }
 
 // Keys per CTA: about 8 waves of 148 CTAs, at least 8 blocks per CTA.
@@ -615,7 +633,7 @@ static int decode_launch(const void* q, const void* k, const void* v, int64_t kv
                          const int64_t* kv_start, const int64_t* kv_len, int64_t batch, int64_t max_kv_len,
                          int32_t hq, int32_t hkv, int32_t head_dim, float scale, const float* k_scale,
                          const float* v_scale, float* o, float* lse, void* workspace, size_t workspace_bytes,
-                         void* stream) {
+                         void* stream, CombineRoute route = CombineRoute{nullptr, nullptr, 1, 0}) {
   using G = DecGeo<kFp8>;
   RCP_CHECK_ARG(head_dim == 128, "head_dim must be 128, got %d", head_dim);
   RCP_CHECK_ARG(hq >= 1 && hkv >= 1 && hq % hkv == 0,
@@ -623,11 +641,12 @@ static int decode_launch(const void* q, const void* k, const void* v, int64_t kv
   RCP_CHECK_ARG(batch >= 0 && max_kv_len >= 0 && kv_rows >= 0, "bad sizes");
   RCP_CHECK_ARG(kv_rows < INT32_MAX, "kv arena rows must fit int32");
   if (batch == 0) return RCP_OK;
-  RCP_CHECK_ARG(q && o && lse && kv_start && kv_len, "null pointer");
+  RCP_CHECK_ARG(q && kv_start && kv_len && ((o && lse) || (route.o_dst && route.lse_dst)), "null pointer");
   const size_t need = rcp_decode_workspace_bytes(batch, hq, max_kv_len);
   RCP_CHECK_ARG(workspace && workspace_bytes >= need, "workspace too small: need %zu", need);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (kv_rows == 0 || max_kv_len == 0) return rcp_fill_empty(o, lse, batch * hq, 128, stream);
+  if ((kv_rows == 0 || max_kv_len == 0) && !route.o_dst) return rcp_fill_empty(o, lse, batch * hq, 128, stream);
+  RCP_CHECK_ARG(kv_rows > 0 && max_kv_len > 0, "routed decode needs a non-empty arena");
   RCP_CHECK_ARG(k && v, "null kv pointer");
   if (kFp8) {
     RCP_CHECK_ARG(k_scale && v_scale, "null k/v scale pointer");
@@ -672,7 +691,7 @@ static int decode_launch(const void* q, const void* k, const void* v, int64_t kv
   RCP_CUDA(cudaGetLastError());
   const int64_t rows = batch * hq;
   decode_combine_kernel<<<static_cast<unsigned>(rows), kCombineWarps * 32, 0, st>>>(
-      prm.part_o, prm.part_lse, rows, n_split, o, lse);
+      prm.part_o, prm.part_lse, rows, n_split, o, lse, route);
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
 }
@@ -812,6 +831,26 @@ extern "C" int rcp_decode_attn_fp8(const void* q, const void* k, const void* v, 
                                    float* o, float* lse, void* workspace, size_t workspace_bytes, void* stream) {
   return decode_launch<true>(q, k, v, kv_row_stride, kv_rows, kv_start, kv_len, batch, max_kv_len, hq, hkv,
                              head_dim, scale, k_scale, v_scale, o, lse, workspace, workspace_bytes, stream);
+}
+
+extern "C" int rcp_decode_attn_routed(const void* q, const void* k, const void* v, int64_t kv_row_stride,
+                                      int64_t kv_rows, const int64_t* kv_start, const int64_t* kv_len,
+                                      int64_t batch, int64_t max_kv_len, int32_t hq, int32_t hkv,
+                                      int32_t head_dim, float scale, const float* k_scale, const float* v_scale,
+                                      float* const* o_dst, float* const* lse_dst, int32_t n_dst,
+                                      int64_t dst_row_offset, void* workspace, size_t workspace_bytes,
+                                      void* stream) {
+  RCP_CHECK_ARG(o_dst && lse_dst && n_dst >= 1 && batch % n_dst == 0 && dst_row_offset >= 0,
+                "bad output routing (batch %lld over %d destinations)", (long long)batch, n_dst);
+  RCP_CHECK_ARG((k_scale == nullptr) == (v_scale == nullptr), "give both k/v scales (e4m3) or neither (bf16)");
+  const CombineRoute route{o_dst, lse_dst, batch / n_dst * hq, dst_row_offset};
+  if (k_scale)
+    return decode_launch<true>(q, k, v, kv_row_stride, kv_rows, kv_start, kv_len, batch, max_kv_len, hq, hkv,
+                               head_dim, scale, k_scale, v_scale, nullptr, nullptr, workspace, workspace_bytes,
+                               stream, route);
+  return decode_launch<false>(q, k, v, kv_row_stride, kv_rows, kv_start, kv_len, batch, max_kv_len, hq, hkv,
+                              head_dim, scale, nullptr, nullptr, nullptr, nullptr, workspace, workspace_bytes,
+                              stream, route);
 }
 
 extern "C" int rcp_kv_quantize_e4m3(void* dst, int64_t dst_row_stride, const int64_t* dst_rows, const void* src,

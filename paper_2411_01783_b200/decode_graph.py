@@ -30,7 +30,7 @@ import torch
 
 from . import _lib
 from .attention import GqaConfig, merge_rows_into
-from .kv_cache import RankKvCache
+from .kv_cache import RankKvCache, _CudaArray
 from .ring import _cuda_decode, merge_order_of
 from .sharding import plan_decode
 
@@ -45,6 +45,86 @@ def _lens_slice(g) -> slice:
 _SCRATCH_SEQ = -7  # cache-internal sequence id of the scratch row (never a query's id)
 
 
+def _align256(x: int) -> int:
+    return (x + 255) // 256 * 256
+
+
+class _PeerDecodeBuffers:
+    """The decode step's exchange buffers in CUDA-IPC memory mapped on every
+    rank (transport="p2p"): per rank one allocation holding
+    q_all [N*S, Hq, D] bf16 | recv_o [N*S, Hq, D] fp32 | recv_l [N*S, Hq] fp32 |
+    flags_q [N] | flags_o [N] (u64 epochs).  Rank k's put stores its query
+    slots into block k of every rank's q_all, its routed decode combine stores
+    the partials of rank s's queries into block k of rank s's recv_o / recv_l,
+    and each phase ends with an epoch signal into slot k of every rank's flags
+    and a wait on its own — the Q all-gather and the All2All without NCCL."""
+
+    def __init__(self, comm, S: int, H: int, D: int, device):
+        import ctypes
+
+        lib = _lib.load()
+        n, k = comm.world, comm.rank
+        R = n * S
+        self.n, self.k, self.S, self.H, self.D = n, k, S, H, D
+        self.off_q = 0
+        self.off_o = _align256(R * H * D * 2)
+        self.off_l = self.off_o + _align256(R * H * D * 4)
+        self.off_fq = self.off_l + _align256(R * H * 4)
+        self.off_fo = self.off_fq + _align256(n * 8)
+        total = self.off_fo + _align256(n * 8)
+        own = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(64)
+        self.device = device
+        with torch.cuda.device(device):
+            _lib.check(lib.rcp_ipc_alloc(total, ctypes.byref(own), handle))
+            self._own = own.value
+            torch.as_tensor(_CudaArray(self._own, (total,), "|u1"), device=device).zero_()
+            torch.cuda.synchronize(device)
+            handles = comm.all_gather_bytes(handle.raw)
+            self.base, self._opened = [], []
+            for r in range(n):
+                if r == k:
+                    self.base.append(self._own)
+                    continue
+                p = ctypes.c_void_p()
+                _lib.check(lib.rcp_ipc_open(handles[r], ctypes.byref(p)))
+                self.base.append(p.value)
+                self._opened.append(p.value)
+            comm.stream_barrier(device)  # every rank's flags are zero before anyone signals
+            torch.cuda.synchronize(device)
+        B = self.base
+        dev_i64 = lambda xs: torch.tensor(xs, dtype=torch.int64, device=device)
+        self.q_dst = dev_i64([B[p] + self.off_q + k * S * H * D * 2 for p in range(n)])
+        self.o_dst = dev_i64([B[p] + self.off_o for p in range(n)])
+        self.l_dst = dev_i64([B[p] + self.off_l for p in range(n)])
+        self.fq_dst = dev_i64([B[p] + self.off_fq + k * 8 for p in range(n)])
+        self.fo_dst = dev_i64([B[p] + self.off_fo + k * 8 for p in range(n)])
+        self.epoch = torch.zeros(1, dtype=torch.int64, device=device)
+        self.timed_out = torch.zeros(1, dtype=torch.int32, device=device)
+        own_t = lambda off, shape, ts: torch.as_tensor(_CudaArray(self._own + off, shape, ts), device=device)
+        self.q_all = own_t(self.off_q, (R, H, D), "<i2").view(torch.bfloat16)
+        self.recv_o = own_t(self.off_o, (R, H, D), "<f4")
+        self.recv_l = own_t(self.off_l, (R, H), "<f4")
+
+    def flags(self, which: str) -> int:
+        return self._own + (self.off_fq if which == "q" else self.off_fo)
+
+    def close(self, comm) -> None:
+        lib = _lib.load()
+        with torch.cuda.device(self.device):
+            torch.cuda.synchronize()
+            comm.stream_barrier(self.device)  # no rank still stores into a peer's buffer
+            torch.cuda.synchronize()
+            for p in self._opened:
+                lib.rcp_ipc_close(p)
+            self._opened = []
+            comm.stream_barrier(self.device)  # every peer unmapped before the owner frees
+            torch.cuda.synchronize()
+            if self._own:
+                lib.rcp_ipc_free(self._own)
+            self._own = 0
+
+
 class GraphedDecode:
     """Replayable decode step for ``batch`` on this rank.
 
@@ -54,9 +134,18 @@ class GraphedDecode:
     (out [slots, Hq, D], lse [slots, Hq]) buffers, valid until the next step.
     """
 
+    TRANSPORTS = ("nccl", "p2p")
+
     def __init__(self, comm, cache: RankKvCache, cfg: GqaConfig, batch, max_steps: int = 256,
                  first_iteration: int = 0, first_positions=None, merge_order: str = "arrival",
-                 grouped_a2a: bool = True):
+                 grouped_a2a: bool = True, transport: str = "nccl"):
+        """``transport``: "nccl" (Q all-gather + grouped All2All through
+        torch.distributed) or "p2p" (N > 1 on one NVLink domain: the Q put and
+        the partials stored straight into the peers' CUDA-IPC buffers by the
+        kernels, with device-side epoch flags; call ``close()`` on every rank
+        together when done)."""
+        if transport not in self.TRANSPORTS:
+            raise ValueError(f"transport must be one of {self.TRANSPORTS}, got {transport!r}")
         if cache.device.type != "cuda":
             raise RuntimeError("GraphedDecode needs the cache on a CUDA device")
         if getattr(cache, "fp8", False) and (cache.k_scale is None or cache.v_scale is None):
@@ -65,6 +154,7 @@ class GraphedDecode:
         merge_order_of(0, 1, merge_order)  # validates the mode
         self.merge_mode = merge_order
         self.grouped_a2a = grouped_a2a
+        self.transport = transport if comm.world > 1 else "nccl"
         self.batch = [int(b) for b in batch]
         self.n, self.rank = comm.world, comm.rank
         self.it = int(first_iteration)
@@ -99,6 +189,7 @@ class GraphedDecode:
         lib = _lib.load()
         self.ws = torch.empty(max(int(lib.rcp_decode_workspace_bytes(R, H, self.max_len)), 32),
                               dtype=torch.uint8, device=dev)
+        self.peer = _PeerDecodeBuffers(comm, S, H, D, dev) if self.transport == "p2p" else None
         self.graph = None
         self._arena_ptr = None
         self._segs_at_capture = None
@@ -177,6 +268,9 @@ class GraphedDecode:
             _cuda_decode(self.q_in, c.k, c.v, starts, lens, self.max_len, self.cfg, self.out, self.lse, self.ws,
                          **c.decode_kwargs())
             return
+        if self.peer is not None:
+            self._launches_p2p(starts, lens)
+            return
         d = self.comm.dist
         d.all_gather_into_tensor(self.q_all, self.q_in, group=self.comm.group)
         _cuda_decode(self.q_all, c.k, c.v, starts, lens, self.max_len, self.cfg, self.part_o, self.part_l,
@@ -195,6 +289,40 @@ class GraphedDecode:
         order = merge_order_of(self.rank, self.n, self.merge_mode)
         merge_rows_into([self.recv_o[s * S:(s + 1) * S] for s in order],
                         [self.recv_l[s * S:(s + 1) * S] for s in order], self.out, self.lse)
+
+    def _launches_p2p(self, starts, lens):
+        """Q put -> epoch barrier -> decode with the combine routed into the
+        owners' receive buffers -> epoch barrier -> merge: no NCCL call."""
+        lib, c, P, S = _lib.load(), self.cache, self.peer, self.slots
+        st, n, H, D = _lib.stream_handle(), self.n, self.cfg.n_query_heads, self.cfg.head_dim
+        _lib.check(lib.rcp_p2p_epoch_advance(_lib.ptr(P.epoch), st))
+        _lib.check(lib.rcp_p2p_put(_lib.ptr(P.q_dst), n, _lib.ptr(self.q_in), S * H * D * 2, st))
+        _lib.check(lib.rcp_p2p_signal(_lib.ptr(P.fq_dst), n, _lib.ptr(P.epoch), st))
+        _lib.check(lib.rcp_p2p_wait(P.flags("q"), n, _lib.ptr(P.epoch), _lib.ptr(P.timed_out), st))
+        ks, vs = c.decode_kwargs().get("scales", (None, None))
+        _lib.count("rcp_decode_attn_routed")
+        _lib.check(lib.rcp_decode_attn_routed(
+            _lib.ptr(P.q_all), _lib.ptr(c.k), _lib.ptr(c.v), c.k.stride(0), c.k.shape[0], _lib.ptr(starts),
+            _lib.ptr(lens), n * S, max(self.max_len, 1), H, self.cfg.n_kv_heads, D, float(self.cfg.scale),
+            _lib.ptr(ks), _lib.ptr(vs), _lib.ptr(P.o_dst), _lib.ptr(P.l_dst), n, self.rank * S * H,
+            _lib.ptr(self.ws), self.ws.numel(), st))
+        _lib.check(lib.rcp_p2p_signal(_lib.ptr(P.fo_dst), n, _lib.ptr(P.epoch), st))
+        _lib.check(lib.rcp_p2p_wait(P.flags("o"), n, _lib.ptr(P.epoch), _lib.ptr(P.timed_out), st))
+        order = merge_order_of(self.rank, n, self.merge_mode)
+        merge_rows_into([P.recv_o[s * S:(s + 1) * S] for s in order],
+                        [P.recv_l[s * S:(s + 1) * S] for s in order], self.out, self.lse)
+
+    def check_transport(self) -> None:
+        """Raise if a p2p wait gave up on a peer (reads a device flag: syncs)."""
+        if self.peer is not None and int(self.peer.timed_out.item()):
+            raise RuntimeError("GraphedDecode: a peer never signalled (p2p wait timed out)")
+
+    def close(self) -> None:
+        """Release the p2p buffers (every rank calls it together)."""
+        if self.peer is not None:
+            self.peer.close(self.comm)
+            self.peer = None
+        self.graph = None
 
     def _capture(self):
         self._launches()  # warm-up: lazy inits, NCCL communicators, function attributes

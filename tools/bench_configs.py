@@ -192,7 +192,8 @@ def run_decode(args, rank, world):
             # consecutive positions per step: the step metadata is precomputed on the
             # device and selected by the graph (no per-step upload / host metadata)
             gd = GraphedDecode(comm, cache, cfg, batch, max_steps=args.warmup + 2 * args.steps + 4,
-                               first_positions=None if args.no_table else pos0, grouped_a2a=not args.separate_a2a)
+                               first_positions=None if args.no_table else pos0, grouped_a2a=not args.separate_a2a,
+                               transport=args.transport)
 
             def step():  # noqa: F811 - graphed variant
                 it = gd.it
@@ -222,8 +223,12 @@ def run_decode(args, rank, world):
                 "config": "cfg5-ring-pass-q-decode", "cp": world, "batch": B, "context": args.context,
                 "q_transport": "allgather" if (args.gather or args.graph) else "ring",
                 "cuda_graph": bool(args.graph), "device_step_table": bool(args.graph and not args.no_table),
+                "transport": args.transport if (args.graph and world > 1) else None,
                 "n_q_heads": hq, "n_kv_heads": hkv, "kv_dtype": args.kv_dtype, "step_ms": ms, "step_ms_back_to_back": b2b,
                 "kv_bytes_per_rank": kv_bytes, "hbm_gbs_effective": kv_bytes / (ms * 1e-3) / 1e9}), flush=True)
+        if args.graph:
+            gd.check_transport()
+            gd.close()
         del cache
         torch.cuda.empty_cache()
 
@@ -246,6 +251,8 @@ def main():
                     help="partial: feed Alg. 1 the attention / link / All2All constants measured in this run")
     ap.add_argument("--fused", action="store_true",
                     help="partial: also time pass-Q with peer-memory partials (no All2All), checked bitwise")
+    ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
+                    help="decode --graph at N > 1: NCCL collectives or kernel stores into CUDA-IPC peer buffers")
     ap.add_argument("--kv-dtype", choices=["bf16", "e4m3"], default="bf16",
                     help="decode: KV-cache storage (e4m3 = FP8 KV, per-head scales calibrated at prefill)")
     ap.add_argument("--steps", type=int, default=5)

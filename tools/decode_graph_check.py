@@ -57,7 +57,8 @@ def main():
         table = os.environ.get("GD_TABLE") == "1"
         gd = GraphedDecode(comm, caches[1], cfg, batch, max_steps=2 * (steps + warm) + 4,
                            first_positions={b: context for b in batch} if table else None,
-                           grouped_a2a=os.environ.get("GD_GROUPED") == "1")
+                           grouped_a2a=os.environ.get("GD_GROUPED") == "1",
+                           transport=os.environ.get("GD_TRANSPORT", "nccl"))
         gq = torch.Generator(device="cuda").manual_seed(7)  # same tokens on every rank
         max_err = 0.0
         t_e, t_g = [], []
@@ -90,10 +91,12 @@ def main():
         stats = torch.tensor([max_err, statistics.median(t_e), statistics.median(t_g)], device="cuda")
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
         if rank == 0:
-            print(f"world {world} B {B} ctx {context} kv={os.environ.get('GD_KV', 'bf16')} table={os.environ.get('GD_TABLE')} "
+            print(f"world {world} B {B} ctx {context} kv={os.environ.get('GD_KV', 'bf16')} transport={os.environ.get('GD_TRANSPORT', 'nccl')} table={os.environ.get('GD_TABLE')} "
                   f"grouped={os.environ.get('GD_GROUPED')}: max |eager - graph| {stats[0].item():.2e}; step eager "
                   f"{stats[1].item():.3f} ms, graph {stats[2].item():.3f} ms", flush=True)
         res.append(stats[0].item())
+        gd.check_transport()
+        gd.close()
         del caches, gd
         torch.cuda.empty_cache()
     assert max(res) < 1e-3, res
