@@ -519,19 +519,16 @@ __global__ void __launch_bounds__(kCombineWarps * 32) decode_combine_kernel(
   if (route.o_dst) __threadfence_system();  // peer stores visible before the step's signal
 }
 
-// Keys per CTA: about 8 waves of 148 CTAs, at least 8 blocks per CTA.
-// CTA-count target of the split heuristic.  148 x 8 (about 2.7 waves of the
-// three CTAs per SM the 2-stage ring allows) measured best: 148 x 6 and
-// 148 x 3 gave 0.79 / 0.87 ms per graphed B=4 step against 0.755 ms.
-// (Round 2: 148 x 9, three full waves of 3 CTAs per SM instead of 2.65, measured
-// neutral at B = 1 (0.247 vs 0.245 ms per graphed step) and 2 % slower at B = 4.)
+// Keys per CTA from a CTA-count target, at least 8 blocks per CTA.  Round 1
+// picked 148 x 8 (about 2.7 waves of the three CTAs per SM the 2-stage ring
+// allows) over 148 x 6 / x 3 with the split index fastest in the grid; with
+// the KV heads fastest (round 2) 148 x 6 — two full waves — is best at every
+// batch of the graphed cfg5 CP4 step: 0.283 / 0.743 / 4.90 ms at B = 1 / 4 /
+// 32 against 0.294 / 0.748 / 4.93 at 148 x 8 and 0.305 / 0.753 / 4.95 at
+// 148 x 10 (profiles/r02_decode_cta_target_sweep.txt).
 #ifndef RCP_DEC_CTA_TARGET
-#define RCP_DEC_CTA_TARGET (148 * 8)
+#define RCP_DEC_CTA_TARGET (148 * 6)
 #endif
-// e4m3: a CTA streams half the bytes per key, so fewer, longer CTAs: 148 x 6
-// (two full waves of three CTAs per SM at B = 1) measured 0.113 ms per B = 1
-// kernel (262144 keys x 8 KV heads) against 0.132 ms at 148 x 8, and 0.41 vs
-// 0.47 ms at B = 4 (profiles/r02_decode_kernel_sweep.jsonl).
 #ifndef RCP_DEC_CTA_TARGET_FP8
 #define RCP_DEC_CTA_TARGET_FP8 (148 * 6)
 #endif
