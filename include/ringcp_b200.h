@@ -166,6 +166,17 @@ int rcp_kv_quantize_e4m3(void* dst, int64_t dst_row_stride, const int64_t* dst_r
  * snapshots and prefill messages built from an e4m3 cache. */
 int rcp_kv_dequantize_e4m3(void* dst, int64_t dst_row_stride, const void* src, int64_t src_row_stride,
                            int64_t n_rows, int32_t hkv, int32_t head_dim, const float* scale, void* stream);
+/* One decode step's cache appends (GraphedDecode): slot j < slots of the
+ * step's new tokens k_in / v_in ([slots, hkv, head_dim] bf16) goes to arena row
+ * meta[j] of the DEVICE step metadata (int64); its position / sequence id
+ * meta[pos_off + j] / meta[seq_off + j] go to pos_arena / seq_arena (int32).
+ * K/V rows are copied (bf16 arenas, k_scale = v_scale = NULL) or quantised as
+ * rcp_kv_quantize_e4m3 (e4m3 arenas).  kv_row_stride in elements. */
+int rcp_decode_append(const int64_t* meta, int32_t slots, int64_t pos_off, int64_t seq_off, const void* k_in,
+                      const void* v_in, void* k_arena, void* v_arena, int64_t kv_row_stride, int32_t hkv,
+                      int32_t head_dim, int32_t* pos_arena, int32_t* seq_arena, const float* k_scale,
+                      const float* v_scale, void* stream);
+
 /* Per-KV-head scale from bf16 rows: scale[h] = max(absmax_h, 2^-24) / 448
  * (fp32 IEEE division) rounded up to a power of two (then e4m3 * scale is
  * exact in bf16: prefill and decode read the same values).  workspace: hkv * 4 bytes of device memory. */

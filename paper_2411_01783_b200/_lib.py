@@ -83,6 +83,9 @@ SIGNATURES = {
         _c_void_p, _i64, _c_void_p, _c_void_p, _i64, _i64, _i32, _i32, _c_void_p, _c_void_p]),
     "rcp_kv_dequantize_e4m3": (ctypes.c_int, [
         _c_void_p, _i64, _c_void_p, _i64, _i64, _i32, _i32, _c_void_p, _c_void_p]),
+    "rcp_decode_append": (ctypes.c_int, [
+        _c_void_p, _i32, _i64, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _i64, _i32, _i32, _c_void_p,
+        _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
     "rcp_kv_calibrate_e4m3": (ctypes.c_int, [
         _c_void_p, _i64, _i64, _i32, _i32, _c_void_p, _c_void_p, _c_void_p]),
 }

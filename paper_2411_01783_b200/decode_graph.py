@@ -257,12 +257,15 @@ class GraphedDecode:
             _lib.check(_lib.load().rcp_step_select(
                 _lib.ptr(self.meta), _lib.ptr(self._table), self.meta.numel(), _lib.ptr(self._counter),
                 self._table.shape[0], _lib.stream_handle()))
-        rows = self.meta[:S]
-        c.store_rows(rows, self.k_in, self.v_in)
         R = self.n * S
-        meta32 = self.meta[S + 2 * R:].to(torch.int32)  # pos | seq of the appends
-        c.pos.index_copy_(0, rows, meta32[:S])
-        c.seq.index_copy_(0, rows, meta32[S:])
+        ks, vs = c.decode_kwargs().get("scales", (None, None))
+        # the owners' appends: K/V rows (copied or e4m3-quantised), positions
+        # and sequence ids of the step metadata, in one launch
+        _lib.count("rcp_decode_append")
+        _lib.check(_lib.load().rcp_decode_append(
+            _lib.ptr(self.meta), S, S + 2 * R, S + 2 * R + S, _lib.ptr(self.k_in), _lib.ptr(self.v_in),
+            c.k.data_ptr(), c.v.data_ptr(), c.k.stride(0), self.cfg.n_kv_heads, self.cfg.head_dim,
+            _lib.ptr(c.pos), _lib.ptr(c.seq), _lib.ptr(ks), _lib.ptr(vs), _lib.stream_handle()))
         starts, lens = self.meta[S:S + R], self.meta[S + R:S + 2 * R]
         if self.n == 1:
             _cuda_decode(self.q_in, c.k, c.v, starts, lens, self.max_len, self.cfg, self.out, self.lse, self.ws,
