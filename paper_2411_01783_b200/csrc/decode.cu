@@ -444,7 +444,10 @@ __global__ void __launch_bounds__(kDecThreads) decode_mma_kernel(const __grid_co
 // exp(lse_s - max), and warp 0 adds the 8 warp sums in warp order.
 // Deterministic; the same kernel serves every decode transport, so they stay
 // bit-identical.
-constexpr int kCombineWarps = 8;
+#ifndef RCP_COMBINE_WARPS
+#define RCP_COMBINE_WARPS 16  // ncu, B=1 / 4 at 262144 keys: 8.2 / 9.2 us (8 warps), 6.6 / 8.7 (16), 5.8 / 11.2 (32)
+#endif
+constexpr int kCombineWarps = RCP_COMBINE_WARPS;
 // Output routing (rcp_decode_attn_routed): with o_dst non-null, row r goes to
 // destination d = r / rows_per_dst (a DEVICE array of base pointers, e.g. the
 // owners' peer-mapped receive buffers), row dst_row_offset + r % rows_per_dst.
