@@ -29,14 +29,6 @@ constexpr uint32_t kKVBytes = kKRows * kD * 2;      // 16 KB: two 8 KB SW128 box
 constexpr uint32_t kKVBoxBytes = kKVBytes / 2;
 constexpr uint32_t kSmemBytes = 2 * kQTileBytes + kSlots * kKVBytes + 1024;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-// Of every 8 score pairs of a FULL block, this many take exp2 on the FMA pipe
-// (cubic polynomial) instead of MUFU.EX2, balancing the two pipes.  With the
-// per-tile MMA issuers (v4f) the softmax waits less and the FMA pipe is the
-// tighter one: 1 measured +3 % over 2 (CP1), 0 and 3 slower.
-#ifndef RCP_POLY_PAIRS
-#define RCP_POLY_PAIRS 1
-#endif
-constexpr int kPolyPairsPer8 = RCP_POLY_PAIRS;
 constexpr uint32_t kTmemO = 0, kTmemS = 256;  // column bases
 
 struct AttnParams {

@@ -102,6 +102,18 @@ __global__ void __launch_bounds__(256) active_list_kernel(const TileSum* __restr
 #ifndef RCP_DBG_NO_EXP
 #define RCP_DBG_NO_EXP 0
 #endif
+// exp2 split of a FULL block: score pair i (of 32) takes the FMA-pipe
+// polynomial when bit i of RCP_POLY_MASK is set.  Round 2 A/B
+// (profiles/r02_k1_ab.txt, same box): pairs {0,1,2,16,17,18} (18.75 %) run
+// +1.5 % over round 1's 1 of 8 ({0,8,16,24}, 12.5 %); the same share spread
+// differently ({0,5,10,16,21,26}: -5 %; {0..5}: -3 %) or 12.5 / 25 % at the
+// half starts ({0,1,16,17}: -2 %; {0..3,16..19}: 0 %) are not — the position
+// of the polynomial pairs in the unrolled loop sets how well the FMA work
+// interleaves with the MUFU stream.
+#ifndef RCP_POLY_MASK
+#define RCP_POLY_MASK 0x00070007u
+#endif
+constexpr uint32_t kPolyMask = RCP_POLY_MASK;
 
 // kPhase (v15, RCP_ATTN_VERSION=15): the two tiles' softmax warps that share
 // an SMSP (warps 4+s and 8+s) run half a block apart — tile 1 starts block j
@@ -368,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             if (RCP_DBG_NO_EXP) {  // bound-finding builds only (tools/dbg_builds.sh)
               p0 = x.x;
               p1 = x.y;
-            } else if ((i & 7) < kPolyPairsPer8) {
+            } else if (kPolyMask & (1u << i)) {
 #if RCP_PACKED_POLY
               const float2 pp = ex2_poly_x2(x.x, x.y);
               p0 = pp.x;
