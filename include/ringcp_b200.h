@@ -146,12 +146,16 @@ int rcp_decode_attn_fp8(const void* q, const void* k, const void* v, int64_t kv_
  * (DEVICE arrays of n_dst base pointers, e.g. the owners' CUDA-IPC receive
  * buffers) at query row dst_row_offset + (b % (batch / n_dst)) — the All2All
  * of Alg. 4 done by the combine kernel's own stores over NVLink.  k_scale /
- * v_scale NULL selects bf16 K/V, non-NULL e4m3. */
+ * v_scale NULL selects bf16 K/V, non-NULL e4m3.  flag_dst non-NULL (DEVICE
+ * array of n_dst flag slots): the combine's last CTA also publishes *epoch
+ * there once every row is stored (as rcp_p2p_signal; counter: a device u32,
+ * zero before the first call, re-armed by the kernel). */
 int rcp_decode_attn_routed(const void* q, const void* k, const void* v, int64_t kv_row_stride,
                            int64_t kv_rows, const int64_t* kv_start, const int64_t* kv_len, int64_t batch,
                            int64_t max_kv_len, int32_t hq, int32_t hkv, int32_t head_dim, float scale,
                            const float* k_scale, const float* v_scale, float* const* o_dst,
-                           float* const* lse_dst, int32_t n_dst, int64_t dst_row_offset, void* workspace,
+                           float* const* lse_dst, int32_t n_dst, int64_t dst_row_offset,
+                           uint64_t* const* flag_dst, uint64_t* epoch, uint32_t* counter, void* workspace,
                            size_t workspace_bytes, void* stream);
 
 /* bf16 rows -> e4m3 rows: row j of src ([n_rows, hkv * head_dim], row stride
@@ -192,14 +196,18 @@ int rcp_cast_f32_bf16(void* dst, const float* src, int64_t n, void* stream);
  * all-gather and partial All2All without NCCL, graph-capturable):
  *   rcp_p2p_epoch_advance: *epoch += 1 (once per step, every rank);
  *   rcp_p2p_put:    copy `bytes` (multiple of 16) of src to each of the n
- *                   destinations dst[0..n) (DEVICE array of pointers);
+ *                   destinations dst[0..n) (DEVICE array of pointers); with
+ *                   flag_dst non-NULL its last block also advances *epoch
+ *                   and publishes it to flag_dst[0..n) (counter: device u32,
+ *                   zero initially, re-armed by the kernel);
  *   rcp_p2p_signal: publish *epoch to each flag_dst[p] (DEVICE array; this
  *                   rank's flag slot in peer p's buffer), release, system scope;
  *   rcp_p2p_wait:   wait until flags[0..n) (this rank's own slots) all reach
  *                   *epoch, acquire; after ~9 s sets *timed_out = 1 and returns
  *                   (the caller checks it) instead of hanging. */
 int rcp_p2p_epoch_advance(uint64_t* epoch, void* stream);
-int rcp_p2p_put(void* const* dst, int32_t n, const void* src, size_t bytes, void* stream);
+int rcp_p2p_put(void* const* dst, int32_t n, const void* src, size_t bytes, uint64_t* const* flag_dst,
+                uint64_t* epoch, uint32_t* counter, void* stream);
 int rcp_p2p_signal(uint64_t* const* flag_dst, int32_t n, const uint64_t* epoch, void* stream);
 int rcp_p2p_wait(const uint64_t* flags, int32_t n, const uint64_t* epoch, int32_t* timed_out, void* stream);
 

@@ -73,10 +73,11 @@ SIGNATURES = {
         _i32, _i32, _i32, _f32, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size_t, _c_void_p]),
     "rcp_decode_attn_routed": (ctypes.c_int, [
         _c_void_p, _c_void_p, _c_void_p, _i64, _i64, _c_void_p, _c_void_p, _i64, _i64,
-        _i32, _i32, _i32, _f32, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _i32, _i64, _c_void_p, _size_t,
-        _c_void_p]),
+        _i32, _i32, _i32, _f32, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _i32, _i64, _c_void_p, _c_void_p,
+        _c_void_p, _c_void_p, _size_t, _c_void_p]),
     "rcp_p2p_epoch_advance": (ctypes.c_int, [_c_void_p, _c_void_p]),
-    "rcp_p2p_put": (ctypes.c_int, [_c_void_p, _i32, _c_void_p, _size_t, _c_void_p]),
+    "rcp_p2p_put": (ctypes.c_int, [_c_void_p, _i32, _c_void_p, _size_t, _c_void_p, _c_void_p, _c_void_p,
+                                    _c_void_p]),
     "rcp_p2p_signal": (ctypes.c_int, [_c_void_p, _i32, _c_void_p, _c_void_p]),
     "rcp_p2p_wait": (ctypes.c_int, [_c_void_p, _i32, _c_void_p, _c_void_p, _c_void_p]),
     "rcp_kv_quantize_e4m3": (ctypes.c_int, [

@@ -336,13 +336,19 @@ static unsigned grid_for(int64_t work, int threads) {
 __global__ void p2p_epoch_kernel(unsigned long long* epoch) { *epoch += 1ull; }
 
 __global__ void __launch_bounds__(256) p2p_put_kernel(void* const* __restrict__ dst, int n,
-                                                      const uint4* __restrict__ src, int64_t n16) {
+                                                      const uint4* __restrict__ src, int64_t n16,
+                                                      unsigned long long* const* flag_dst,
+                                                      unsigned long long* epoch, unsigned* counter) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n16;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint4 v = __ldg(src + i);
     for (int p = 0; p < n; ++p) reinterpret_cast<uint4*>(dst[p])[i] = v;
   }
-  __threadfence_system();
+  if (flag_dst) {
+    p2p_last_block_signal(counter, flag_dst, n, epoch, true);  // advance the epoch, then signal
+  } else {
+    __threadfence_system();
+  }
 }
 
 __global__ void p2p_signal_kernel(unsigned long long* const* __restrict__ flag_dst, int n,
@@ -540,14 +546,18 @@ int rcp_p2p_epoch_advance(uint64_t* epoch, void* stream) {
   return RCP_OK;
 }
 
-int rcp_p2p_put(void* const* dst, int32_t n, const void* src, size_t bytes, void* stream) {
+int rcp_p2p_put(void* const* dst, int32_t n, const void* src, size_t bytes, uint64_t* const* flag_dst,
+                uint64_t* epoch, uint32_t* counter, void* stream) {
   RCP_CHECK_ARG(dst && src && n >= 1 && bytes % 16 == 0, "bad p2p put (bytes %% 16 == 0, n >= 1)");
   RCP_CHECK_ARG((reinterpret_cast<uintptr_t>(src) & 15) == 0, "src must be 16-byte aligned");
+  RCP_CHECK_ARG(!flag_dst || (epoch && counter), "a signalling put needs the epoch and a counter");
   const int64_t n16 = static_cast<int64_t>(bytes / 16);
+  RCP_CHECK_ARG(n16 > 0 || !flag_dst, "a signalling put needs data");
   if (n16 == 0) return RCP_OK;
   const int64_t blocks = (n16 + 255) / 256;
   p2p_put_kernel<<<static_cast<unsigned>(blocks < 296 ? blocks : 296), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      dst, n, static_cast<const uint4*>(src), n16);
+      dst, n, static_cast<const uint4*>(src), n16, reinterpret_cast<unsigned long long* const*>(flag_dst),
+      reinterpret_cast<unsigned long long*>(epoch), counter);
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
 }

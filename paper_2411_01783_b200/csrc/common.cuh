@@ -67,6 +67,33 @@ __device__ __forceinline__ float merge_val(float a, float b, const MergeW& w) {
   return __fadd_rn(__fmul_rn(a, w.wa), __fmul_rn(b, w.wb));
 }
 
+// ------------------------------------------------------------------ P2P completion signal
+// Called by EVERY thread of every block of a grid after the block's peer
+// stores: the last block to arrive (device counter, re-armed here) publishes
+// the step epoch — first advanced by one if `advance` — into each of the n
+// peers' flag slots (release, system scope).  Fuses the separate signal kernel
+// of the decode step's p2p transport into the kernel that did the stores.
+__device__ __forceinline__ void p2p_last_block_signal(unsigned* counter, unsigned long long* const* flag_dst,
+                                                      int n, unsigned long long* epoch, bool advance) {
+  __shared__ int s_last;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    s_last = atomicAdd(counter, 1u) == gridDim.x * gridDim.y * gridDim.z - 1 ? 1 : 0;
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    *counter = 0u;
+    unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(epoch);
+    if (advance) {
+      e += 1ull;
+      *reinterpret_cast<volatile unsigned long long*>(epoch) = e;
+    }
+    __threadfence_system();
+    for (int p = 0; p < n; ++p)
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag_dst[p]), "l"(e) : "memory");
+  }
+}
+
 // ------------------------------------------------------------------ tile summaries
 // Per 64- or 128-token tile of a block: min/max position and sequence id over the
 // VALID rows, number of valid rows, and whether all rows are valid and of

@@ -456,6 +456,12 @@ struct CombineRoute {
   float* const* lse_dst;
   int64_t rows_per_dst;
   int64_t dst_row_offset;
+  // optional completion signal (the p2p transport): the last CTA publishes
+  // *epoch into each flag_dst[p] once every routed row is stored
+  unsigned long long* const* flag_dst;
+  int n_flags;
+  unsigned long long* epoch;
+  unsigned* counter;
 };
 
 __global__ void __launch_bounds__(kCombineWarps * 32) decode_combine_kernel(
@@ -497,7 +503,7 @@ __global__ void __launch_bounds__(kCombineWarps * 32) decode_combine_kernel(
   s_acc[warp][lane] = acc;
   if (lane == 0) s_l[warp] = l;
   __syncthreads();
-  if (warp != 0) return;
+  if (warp == 0) {
   float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
   float lt = 0.f;
 #pragma unroll
@@ -520,7 +526,12 @@ __global__ void __launch_bounds__(kCombineWarps * 32) decode_combine_kernel(
   }
   reinterpret_cast<float4*>(orow)[lane] = make_float4(r.x * inv, r.y * inv, r.z * inv, r.w * inv);
   if (lane == 0) *lrow = has ? mt + logf(lt) : -INFINITY;
-  if (route.o_dst) __threadfence_system();  // peer stores visible before the step's signal
+  }
+  if (route.flag_dst) {
+    p2p_last_block_signal(route.counter, route.flag_dst, route.n_flags, route.epoch, false);
+  } else if (route.o_dst) {
+    __threadfence_system();  // peer stores visible before the step's signal
+  }
 }
 
 // Keys per CTA from a CTA-count target, at least 8 blocks per CTA.  Round 1
@@ -634,7 +645,7 @@ static int decode_launch(const void* q, const void* k, const void* v, int64_t kv
                          const int64_t* kv_start, const int64_t* kv_len, int64_t batch, int64_t max_kv_len,
                          int32_t hq, int32_t hkv, int32_t head_dim, float scale, const float* k_scale,
                          const float* v_scale, float* o, float* lse, void* workspace, size_t workspace_bytes,
-                         void* stream, CombineRoute route = CombineRoute{nullptr, nullptr, 1, 0}) {
+                         void* stream, CombineRoute route = CombineRoute{nullptr, nullptr, 1, 0, nullptr, 0, nullptr, nullptr}) {
   using G = DecGeo<kFp8>;
   RCP_CHECK_ARG(head_dim == 128, "head_dim must be 128, got %d", head_dim);
   RCP_CHECK_ARG(hq >= 1 && hkv >= 1 && hq % hkv == 0,
@@ -880,12 +891,16 @@ extern "C" int rcp_decode_attn_routed(const void* q, const void* k, const void* 
                                       int64_t batch, int64_t max_kv_len, int32_t hq, int32_t hkv,
                                       int32_t head_dim, float scale, const float* k_scale, const float* v_scale,
                                       float* const* o_dst, float* const* lse_dst, int32_t n_dst,
-                                      int64_t dst_row_offset, void* workspace, size_t workspace_bytes,
+                                      int64_t dst_row_offset, uint64_t* const* flag_dst, uint64_t* epoch,
+                                      uint32_t* counter, void* workspace, size_t workspace_bytes,
                                       void* stream) {
   RCP_CHECK_ARG(o_dst && lse_dst && n_dst >= 1 && batch % n_dst == 0 && dst_row_offset >= 0,
                 "bad output routing (batch %lld over %d destinations)", (long long)batch, n_dst);
   RCP_CHECK_ARG((k_scale == nullptr) == (v_scale == nullptr), "give both k/v scales (e4m3) or neither (bf16)");
-  const CombineRoute route{o_dst, lse_dst, batch / n_dst * hq, dst_row_offset};
+  RCP_CHECK_ARG(!flag_dst || (epoch && counter), "a signalling decode needs the epoch and a counter");
+  const CombineRoute route{o_dst, lse_dst, batch / n_dst * hq, dst_row_offset,
+                           reinterpret_cast<unsigned long long* const*>(flag_dst), n_dst,
+                           reinterpret_cast<unsigned long long*>(epoch), counter};
   if (k_scale)
     return decode_launch<true>(q, k, v, kv_row_stride, kv_rows, kv_start, kv_len, batch, max_kv_len, hq, hkv,
                                head_dim, scale, k_scale, v_scale, nullptr, nullptr, workspace, workspace_bytes,

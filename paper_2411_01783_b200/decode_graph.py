@@ -101,6 +101,7 @@ class _PeerDecodeBuffers:
         self.fo_dst = dev_i64([B[p] + self.off_fo + k * 8 for p in range(n)])
         self.epoch = torch.zeros(1, dtype=torch.int64, device=device)
         self.timed_out = torch.zeros(1, dtype=torch.int32, device=device)
+        self.counters = torch.zeros(2, dtype=torch.int32, device=device)  # last-block counters: put, combine
         own_t = lambda off, shape, ts: torch.as_tensor(_CudaArray(self._own + off, shape, ts), device=device)
         self.q_all = own_t(self.off_q, (R, H, D), "<i2").view(torch.bfloat16)
         self.recv_o = own_t(self.off_o, (R, H, D), "<f4")
@@ -294,13 +295,14 @@ class GraphedDecode:
                         [self.recv_l[s * S:(s + 1) * S] for s in order], self.out, self.lse)
 
     def _launches_p2p(self, starts, lens):
-        """Q put -> epoch barrier -> decode with the combine routed into the
-        owners' receive buffers -> epoch barrier -> merge: no NCCL call."""
+        """Q put (its last block advances the epoch and signals) -> wait ->
+        decode with the combine routed into the owners' receive buffers (its
+        last CTA signals) -> wait -> merge: no NCCL call, five launches."""
         lib, c, P, S = _lib.load(), self.cache, self.peer, self.slots
         st, n, H, D = _lib.stream_handle(), self.n, self.cfg.n_query_heads, self.cfg.head_dim
-        _lib.check(lib.rcp_p2p_epoch_advance(_lib.ptr(P.epoch), st))
-        _lib.check(lib.rcp_p2p_put(_lib.ptr(P.q_dst), n, _lib.ptr(self.q_in), S * H * D * 2, st))
-        _lib.check(lib.rcp_p2p_signal(_lib.ptr(P.fq_dst), n, _lib.ptr(P.epoch), st))
+        cnt = P.counters.data_ptr()
+        _lib.check(lib.rcp_p2p_put(_lib.ptr(P.q_dst), n, _lib.ptr(self.q_in), S * H * D * 2, _lib.ptr(P.fq_dst),
+                                   _lib.ptr(P.epoch), cnt, st))
         _lib.check(lib.rcp_p2p_wait(P.flags("q"), n, _lib.ptr(P.epoch), _lib.ptr(P.timed_out), st))
         ks, vs = c.decode_kwargs().get("scales", (None, None))
         _lib.count("rcp_decode_attn_routed")
@@ -308,8 +310,7 @@ class GraphedDecode:
             _lib.ptr(P.q_all), _lib.ptr(c.k), _lib.ptr(c.v), c.k.stride(0), c.k.shape[0], _lib.ptr(starts),
             _lib.ptr(lens), n * S, max(self.max_len, 1), H, self.cfg.n_kv_heads, D, float(self.cfg.scale),
             _lib.ptr(ks), _lib.ptr(vs), _lib.ptr(P.o_dst), _lib.ptr(P.l_dst), n, self.rank * S * H,
-            _lib.ptr(self.ws), self.ws.numel(), st))
-        _lib.check(lib.rcp_p2p_signal(_lib.ptr(P.fo_dst), n, _lib.ptr(P.epoch), st))
+            _lib.ptr(P.fo_dst), _lib.ptr(P.epoch), cnt + 4, _lib.ptr(self.ws), self.ws.numel(), st))
         _lib.check(lib.rcp_p2p_wait(P.flags("o"), n, _lib.ptr(P.epoch), _lib.ptr(P.timed_out), st))
         order = merge_order_of(self.rank, n, self.merge_mode)
         merge_rows_into([P.recv_o[s * S:(s + 1) * S] for s in order],
