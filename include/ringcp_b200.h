@@ -70,6 +70,18 @@ int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k, int64_t k_r
                  float* lse, int32_t mode, void* workspace, size_t workspace_bytes,
                  void* stream);
 
+/* rcp_attn_fwd with Q and K in e4m3 (OCP; value = scale * e4m3, one fp32
+ * scale per query head in q_scale[hq] and per KV head in k_scale[hkv], device
+ * arrays) and S = Q K^T on the tensor cores' 8-bit path (tcgen05 kind::f8f6f4);
+ * V bf16, P bf16, outputs as rcp_attn_fwd.  Row strides in elements (= bytes
+ * for q8 / k8, multiples of 16).  Opt-in FP8 mode: the
+ * result is rcp_attn_fwd's on the dequantised Q / K. */
+int rcp_attn_fwd_qk8(const void* q8, int64_t q_row_stride, const void* k8, int64_t k_row_stride, const void* v,
+                     int64_t v_row_stride, const int32_t* q_pos, const int32_t* q_seq, const int32_t* k_pos,
+                     const int32_t* k_seq, int64_t tq, int64_t tk, int32_t hq, int32_t hkv, int32_t head_dim,
+                     float scale, const float* q_scale, const float* k_scale, float* o, float* lse, int32_t mode,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
 /* Left-fold merge of n partials (ascending list order), replacing
  * ringcp.attention.merge_attention (attention.py:319-334).  o_parts / lse_parts
  * are HOST arrays of n DEVICE pointers, each O [rows, head_dim] fp32 and LSE

@@ -14,7 +14,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "_ringcp_b200.so")
-SOURCES = ["capi.cu", "attn_fwd.cu", "decode.cu"]
+SOURCES = ["capi.cu", "attn_fwd.cu", "attn_fwd_qk8.cu", "decode.cu"]
 # The A/B library: the same ABI plus the measured alternative attention forms
 # (v12-v17, selected by RCP_ATTN_VERSION).  Not the product:
 # loaded only through RCP_LIB_PATH by tests/test_gpu_variants.py and tools/.

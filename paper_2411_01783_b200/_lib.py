@@ -64,6 +64,10 @@ SIGNATURES = {
     "rcp_fold_meta": (ctypes.c_int, [
         _c_void_p, _c_void_p, _c_void_p, _i64, _i32, _c_void_p, _c_void_p, _c_void_p]),
     "rcp_attn_version": (_i32, []),
+    "rcp_attn_fwd_qk8": (ctypes.c_int, [
+        _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
+        _i64, _i64, _i32, _i32, _i32, _f32, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _i32, _c_void_p, _size_t,
+        _c_void_p]),
     "rcp_decode_workspace_bytes": (_size_t, [_i64, _i32, _i64]),
     "rcp_decode_attn": (ctypes.c_int, [
         _c_void_p, _c_void_p, _c_void_p, _i64, _i64, _c_void_p, _c_void_p, _i64, _i64,

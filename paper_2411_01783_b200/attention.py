@@ -322,6 +322,73 @@ def attend_into(q_data: torch.Tensor, q_meta, k_data: torch.Tensor, v_data: torc
         _lib.stream_handle(stream)))
 
 
+def quantize_heads_e4m3(x: torch.Tensor, scale: torch.Tensor | None = None):
+    """bf16 [T, H, 128] -> (e4m3 bytes [T, H, 128] uint8, per-head fp32 scales
+    [H]): scales absmax / 448 rounded up to a power of two unless given
+    (rcp_kv_calibrate_e4m3 / rcp_kv_quantize_e4m3)."""
+    lib = _lib.load()
+    x = _bf16(x)
+    T, H, D = x.shape
+    rows = x.reshape(T, H * D).contiguous()
+    if scale is None:
+        scale = torch.empty(H, dtype=torch.float32, device=x.device)
+        ws = torch.empty(H, dtype=torch.int32, device=x.device)
+        _lib.count("rcp_kv_calibrate_e4m3")
+        _lib.check(lib.rcp_kv_calibrate_e4m3(_lib.ptr(rows), H * D, T, H, D, _lib.ptr(scale), _lib.ptr(ws),
+                                             _lib.stream_handle()))
+    out = torch.empty((T, H, D), dtype=torch.uint8, device=x.device)
+    _lib.count("rcp_kv_quantize_e4m3")
+    _lib.check(lib.rcp_kv_quantize_e4m3(_lib.ptr(out), H * D, 0, _lib.ptr(rows), H * D, T, H, D, _lib.ptr(scale),
+                                        _lib.stream_handle()))
+    return out, scale
+
+
+def attend_into_qk8(q8: torch.Tensor, q_scale: torch.Tensor, q_meta, k8: torch.Tensor, k_scale: torch.Tensor,
+                    v_data: torch.Tensor, k_meta, n_q_heads: int, n_kv_heads: int, scale: float,
+                    out: torch.Tensor, lse: torch.Tensor, mode: int, workspace: torch.Tensor | None = None,
+                    stream=None) -> None:
+    """Raw call of the FP8-QK attention kernel (rcp_attn_fwd_qk8): e4m3 Q / K
+    [T, H, 128] with per-head scales (value = scale * e4m3), bf16 V, folded
+    int32 metadata, fp32 outputs written in place."""
+    lib = _lib.load()
+    tq, tk = q8.shape[0], k8.shape[0]
+    need = lib.rcp_attn_workspace_bytes(tq, tk)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 32), dtype=torch.uint8, device=q8.device)
+    _lib.count("rcp_attn_fwd")
+    _lib.check(lib.rcp_attn_fwd_qk8(
+        _lib.ptr(q8), q8.stride(0), _lib.ptr(k8), k8.stride(0), _lib.ptr(v_data), v_data.stride(0),
+        _lib.ptr(q_meta[0]), _lib.ptr(q_meta[1]), _lib.ptr(k_meta[0]), _lib.ptr(k_meta[1]),
+        tq, tk, n_q_heads, n_kv_heads, q8.shape[2], float(scale), _lib.ptr(q_scale), _lib.ptr(k_scale),
+        _lib.ptr(out), _lib.ptr(lse), mode, _lib.ptr(workspace), workspace.numel(), _lib.stream_handle(stream)))
+
+
+def gqa_attention_fp8(q: EmbeddingBlock, k: EmbeddingBlock, v: EmbeddingBlock, cfg: GqaConfig,
+                      q_scale: torch.Tensor | None = None, k_scale: torch.Tensor | None = None) -> PartialAttention:
+    """``gqa_attention`` with Q and K quantised to e4m3 (per head) and S = QK^T
+    on the tensor cores' 8-bit path (an opt-in mode outside
+    the bf16 parity contract: its result is that of ``gqa_attention`` on the
+    dequantised Q / K).  head_dim must be 128."""
+    if q.n_heads != cfg.n_query_heads or q.head_dim != cfg.head_dim:
+        raise ValueError(f"query block is [{q.n_heads} x {q.head_dim}] but config wants "
+                         f"[{cfg.n_query_heads} x {cfg.head_dim}]")
+    _check_kv_pair(k, v, cfg)
+    if cfg.head_dim != KERNEL_HEAD_DIM:
+        raise ValueError(f"the e4m3 Q/K kernel takes head_dim == {KERNEL_HEAD_DIM}, got {cfg.head_dim}")
+    if k.n_valid < k.n_tokens:
+        k, v = k.valid_only(), v.valid_only()
+    tq = q.n_tokens
+    dev = q.data.device
+    q8, qs = quantize_heads_e4m3(q.data, q_scale)
+    k8, ks = quantize_heads_e4m3(k.data, k_scale)
+    out = torch.empty((tq, cfg.n_query_heads, KERNEL_HEAD_DIM), dtype=torch.float32, device=dev)
+    lse = torch.empty((tq, cfg.n_query_heads), dtype=torch.float32, device=dev)
+    attend_into_qk8(q8, qs, q.meta32("q"), k8, ks, _bf16(v.data), k.meta32("k"), cfg.n_query_heads,
+                    cfg.n_kv_heads, cfg.scale, out, lse, _lib.MODE_OVERWRITE)
+    blk = EmbeddingBlock(out, q.positions, q.valid, q.seq_ids, validate=False, n_valid=q.n_valid)
+    return PartialAttention(output=blk, lse=lse)
+
+
 def gqa_attention(q: EmbeddingBlock, k: EmbeddingBlock, v: EmbeddingBlock, cfg: GqaConfig) -> PartialAttention:
     """Causal GQA attention of a query block against one key/value block
     (attention.py:230-282) on the tcgen05 kernel.  Key j is admitted for query i

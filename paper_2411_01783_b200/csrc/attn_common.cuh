@@ -52,6 +52,8 @@ struct AttnParams {
   long long* trace;  // RCP_TRACE builds only: per-CTA role timestamps (clock64)
   int* item_ctr;     // v9: work-item counter (workspace, zeroed by active_list_kernel)
   int mask_shift;    // negative-control hook (RCP_FAULT=mask_diag): 1 excludes key == query; else 0
+  const float* q_scale;  // e4m3 Q / K form (attn_fwd_qk8.cu): per query head / per KV head
+  const float* k_scale;
 };
 
 #ifndef RCP_TRACE
@@ -159,6 +161,7 @@ constexpr int kDefaultAttnVersion = RCP_DEFAULT_ATTN_VERSION;
 #define RCP_AB_FORMS 0  // 1: the A/B build with the alternative kernel forms (v12-v17)
 #endif
 int attn_n128_launch(const AttnParams& prm, int64_t grid, cudaStream_t st, int form);
+int attn_qk8_launch(const AttnParams& prm, int64_t grid, cudaStream_t st);
 int attn_pair_launch(const AttnParams& prm, int64_t n_pairs_heads, cudaStream_t st, bool col_split);
 
 }  // namespace rcp

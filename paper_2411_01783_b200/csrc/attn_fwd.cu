@@ -531,18 +531,20 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D map over a token-major [rows, heads*128] bf16 array; box = box_rows x 64 cols, SW128.
+// (e4m3 = true: a [rows, heads*128] e4m3 array, box = box_rows x 128 cols.)
 static int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols,
-                    int64_t row_stride_elems, uint32_t box_rows) {
+                    int64_t row_stride_elems, uint32_t box_rows, bool e4m3 = false) {
   auto fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return RCP_ERR_CUDA;
   }
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_stride_elems) * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_stride_elems) * (e4m3 ? 1 : 2)};
+  cuuint32_t box[2] = {e4m3 ? 128u : 64u, box_rows};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+  CUresult r = fn(m, e4m3 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(base), dims, strides,
                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -588,13 +590,15 @@ extern "C" size_t rcp_attn_workspace_bytes(int64_t tq, int64_t tk) {
   return static_cast<size_t>((nq + nk) * sizeof(TileSum) + nqb * nk * 4 + nqb * 4 + 256);
 }
 
-extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
-                            int64_t k_row_stride, const void* v, int64_t v_row_stride,
-                            const int32_t* q_pos, const int32_t* q_seq, const int32_t* k_pos,
-                            const int32_t* k_seq, int64_t tq, int64_t tk, int32_t hq,
-                            int32_t hkv, int32_t head_dim, float scale, float* o, float* lse,
-                            int32_t mode, void* workspace, size_t workspace_bytes, void* stream) {
+// Shared host side of rcp_attn_fwd and rcp_attn_fwd_qk8 (q_scale non-null:
+// q / k are e4m3 with per-head scales, the attn_fwd_qk8.cu kernel runs).
+static int attn_fwd_host(const void* q, int64_t q_row_stride, const void* k, int64_t k_row_stride, const void* v,
+                         int64_t v_row_stride, const int32_t* q_pos, const int32_t* q_seq, const int32_t* k_pos,
+                         const int32_t* k_seq, int64_t tq, int64_t tk, int32_t hq, int32_t hkv, int32_t head_dim,
+                         float scale, const float* q_scale, const float* k_scale, float* o, float* lse,
+                         int32_t mode, void* workspace, size_t workspace_bytes, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool qk8 = q_scale != nullptr;
   RCP_CHECK_ARG(head_dim == kD, "head_dim must be 128, got %d", head_dim);
   RCP_CHECK_ARG(hq >= 1 && hkv >= 1, "head counts must be positive");
   RCP_CHECK_ARG(hq % hkv == 0, "n_query_heads=%d not divisible by n_kv_heads=%d", hq, hkv);
@@ -608,8 +612,9 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
     return rcp_fill_empty(o, lse, tq * hq, head_dim, stream);
   }
   RCP_CHECK_ARG(q && k && v && k_pos && k_seq, "null pointer");
-  RCP_CHECK_ARG(q_row_stride % 8 == 0 && k_row_stride % 8 == 0 && v_row_stride % 8 == 0,
-                "row strides must be multiples of 8 elements");
+  RCP_CHECK_ARG(q_row_stride % (qk8 ? 16 : 8) == 0 && k_row_stride % (qk8 ? 16 : 8) == 0 && v_row_stride % 8 == 0,
+                "row strides must be multiples of 8 elements (16 for e4m3 q / k)");
+  RCP_CHECK_ARG(!qk8 || k_scale, "e4m3 q / k need both scale arrays");
   RCP_CHECK_ARG(q_row_stride >= hq * kD && k_row_stride >= hkv * kD && v_row_stride >= hkv * kD,
                 "row stride smaller than heads*head_dim");
   RCP_CHECK_ARG(((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) |
@@ -623,16 +628,18 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
                 "workspace too small: need %zu bytes", need);
   RCP_CHECK_ARG((reinterpret_cast<uintptr_t>(workspace) & 31) == 0, "workspace must be 32-byte aligned");
 
-  const int version = attn_version();
+  const int version = qk8 ? kDefaultAttnVersion : attn_version();
   const int krows = attn_key_rows(version);
   AttnParams prm;
   memset(&prm, 0, sizeof(prm));
   int rc;
-  if ((rc = make_map(&prm.tm_q, q, tq, static_cast<int64_t>(hq) * kD, q_row_stride, kQRows)) != RCP_OK)
+  if ((rc = make_map(&prm.tm_q, q, tq, static_cast<int64_t>(hq) * kD, q_row_stride, kQRows, qk8)) != RCP_OK)
     return rc;
   if ((rc = make_map(&prm.tm_k, k, tk, static_cast<int64_t>(hkv) * kD, k_row_stride,
-                     attn_k_box_rows(version))) != RCP_OK)
+                     attn_k_box_rows(version), qk8)) != RCP_OK)
     return rc;
+  prm.q_scale = q_scale;
+  prm.k_scale = k_scale;
   if ((rc = make_map(&prm.tm_v, v, tk, static_cast<int64_t>(hkv) * kD, v_row_stride,
                      attn_v_box_rows(version))) != RCP_OK)
     return rc;
@@ -679,6 +686,7 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
 
   const int64_t grid = static_cast<int64_t>(prm.n_qblk) * hq;
   RCP_CHECK_ARG(grid < (1ll << 30), "grid too large");
+  if (qk8) return attn_qk8_launch(prm, grid, st);
 #if RCP_AB_FORMS
   if (version == 13 || version == 14) {
     if ((rc = attn_pair_launch(prm, grid, st, version == 14)) != RCP_OK) return rc;
@@ -709,6 +717,27 @@ extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
   attn_fwd_kernel<0><<<static_cast<unsigned>(grid), kThreads, kSmemBytes, st>>>(prm);
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
+}
+
+extern "C" int rcp_attn_fwd(const void* q, int64_t q_row_stride, const void* k,
+                            int64_t k_row_stride, const void* v, int64_t v_row_stride,
+                            const int32_t* q_pos, const int32_t* q_seq, const int32_t* k_pos,
+                            const int32_t* k_seq, int64_t tq, int64_t tk, int32_t hq,
+                            int32_t hkv, int32_t head_dim, float scale, float* o, float* lse,
+                            int32_t mode, void* workspace, size_t workspace_bytes, void* stream) {
+  return attn_fwd_host(q, q_row_stride, k, k_row_stride, v, v_row_stride, q_pos, q_seq, k_pos, k_seq, tq, tk, hq,
+                       hkv, head_dim, scale, nullptr, nullptr, o, lse, mode, workspace, workspace_bytes, stream);
+}
+
+extern "C" int rcp_attn_fwd_qk8(const void* q8, int64_t q_row_stride, const void* k8, int64_t k_row_stride,
+                                const void* v, int64_t v_row_stride, const int32_t* q_pos, const int32_t* q_seq,
+                                const int32_t* k_pos, const int32_t* k_seq, int64_t tq, int64_t tk, int32_t hq,
+                                int32_t hkv, int32_t head_dim, float scale, const float* q_scale,
+                                const float* k_scale, float* o, float* lse, int32_t mode, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+  RCP_CHECK_ARG(q_scale && k_scale, "null q / k scale arrays");
+  return attn_fwd_host(q8, q_row_stride, k8, k_row_stride, v, v_row_stride, q_pos, q_seq, k_pos, k_seq, tq, tk, hq,
+                       hkv, head_dim, scale, q_scale, k_scale, o, lse, mode, workspace, workspace_bytes, stream);
 }
 
 extern "C" int rcp_attn_version(void) { return rcp::attn_version(); }

@@ -9,6 +9,7 @@ timed per launch with CUDA events on the launching stream (median of
 pairs) for every implementation, clocks sampled during each timed loop.
 
   ours    rcp_attn_fwd (this repo's tcgen05 kernel, fp32 O + LSE)
+  ours_qk8  rcp_attn_fwd_qk8 (the opt-in FP8 mode: e4m3 Q / K, S on kind::f8f6f4; not bf16)
   fa4     FlashAttention-4 (CuTe DSL, flash_fwd_sm100) as vendored in vllm
   trtllm  flashinfer trtllm-gen precompiled sm100a FMHA (paged KV, NHD pages of 128)
   cudnn   torch SDPA with the cuDNN backend (K/V expanded to Hq heads if GQA is rejected)
@@ -100,6 +101,21 @@ def main():
         ref_rows["ours"] = o[rows].clone()
         if "ours" in which:
             report("ours", ours)
+        if "ours_qk8" in which:
+            # the opt-in FP8 mode: e4m3 Q / K (quantised once, outside the timed
+            # launches, as a model would keep them), S on kind::f8f6f4
+            from paper_2411_01783_b200.attention import attend_into_qk8, quantize_heads_e4m3
+
+            q8, qs = quantize_heads_e4m3(q)
+            k8, ks = quantize_heads_e4m3(k)
+            o8 = torch.empty_like(o)
+            l8 = torch.empty_like(lse)
+
+            def ours_qk8():
+                attend_into_qk8(q8, qs, (pos, seq), k8, ks, v, (pos, seq), hq, hkv, scale, o8, l8,
+                                _lib.MODE_OVERWRITE, workspace=ws)
+
+            report("ours_qk8", ours_qk8, out_rows=lambda: o8[rows])
 
     if "fa4" in which:
         try:
