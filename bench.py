@@ -276,6 +276,42 @@ def cfg1_gpu_run(rc, dev) -> dict:
                     "(sharding + appends + 4 attention launches + merges; median of 10, CUDA events)"}
 
 
+def fp8_qk_run(tens, cfg, dev) -> dict:
+    """The opt-in FP8-QK attention (e4m3 Q / K, S on tcgen05 kind::f8f6f4) at
+    the CP1 shape of the workload: one causal launch over all T tokens, CUDA
+    events, median of 3 after a warm-up.  Reported beside the bf16 headline,
+    never as it."""
+    import torch
+
+    from paper_2411_01783_b200 import _lib
+    from paper_2411_01783_b200.attention import attend_into_qk8, quantize_heads_e4m3
+
+    T, hq, hkv = cfg["T"], cfg["hq"], cfg["hkv"]
+    q8, qs = quantize_heads_e4m3(tens["q"])
+    k8, ks = quantize_heads_e4m3(tens["k"])
+    pos = torch.arange(T, device=dev, dtype=torch.int32)
+    seq = torch.zeros(T, device=dev, dtype=torch.int32)
+    o = torch.empty(T, hq, D, device=dev, dtype=torch.float32)
+    lse = torch.empty(T, hq, device=dev, dtype=torch.float32)
+    ws = torch.empty(_lib.load().rcp_attn_workspace_bytes(T, T), dtype=torch.uint8, device=dev)
+    run = lambda: attend_into_qk8(q8, qs, (pos, seq), k8, ks, tens["v"], (pos, seq), hq, hkv,  # noqa: E731
+                                  D ** -0.5, o, lse, _lib.MODE_OVERWRITE, workspace=ws)
+    run()
+    times = []
+    for _ in range(3):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        run()
+        e.record()
+        torch.cuda.synchronize()
+        times.append(s.elapsed_time(e))
+    ms = statistics.median(times)
+    flops = 4.0 * D * hq * T * (T + 1) / 2
+    return {"value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms": ms,
+            "what": "opt-in FP8-QK attention (rcp_attn_fwd_qk8: e4m3 Q/K per-head scales, P/V bf16), one causal "
+                    "launch at the CP1 shape; NOT the bf16 headline"}
+
+
 def run_reference(args, cfg, rank, world):
     """--impl reference: the reference algorithm (oracle port; the reference is
     pure Python/numpy) on the host cores, rank 0 only."""
@@ -545,6 +581,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_port(T, hq, hkv, rows=args.cpu_rows)
     cfg1 = cfg1_gpu_run(rc, dev) if (rank == 0 and not args.no_cfg1) else None
+    fp8_qk = fp8_qk_run(tens, cfg, dev) if (world == 1 and K == 1 and not args.no_cfg1) else None
     value = flops_total / (ms * 1e-3) / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
@@ -564,6 +601,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "e2e": e2e,
         "exposed_comm": exposed,
         "cfg1": cfg1,
+        "fp8_qk": fp8_qk,
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
