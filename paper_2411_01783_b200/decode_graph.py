@@ -143,8 +143,8 @@ class GraphedDecode:
         """``transport``: "nccl" (Q all-gather + grouped All2All through
         torch.distributed) or "p2p" (N > 1 on one NVLink domain: the Q put and
         the partials stored straight into the peers' CUDA-IPC buffers by the
-        kernels, with device-side epoch flags; call ``close()`` on every rank
-        together when done)."""
+        kernels, with device-side epoch flags; construct it and call
+        ``close()`` on every rank together — both are collective)."""
         if transport not in self.TRANSPORTS:
             raise ValueError(f"transport must be one of {self.TRANSPORTS}, got {transport!r}")
         if cache.device.type != "cuda":
