@@ -215,8 +215,9 @@ int rcp_cast_f32_bf16(void* dst, const float* src, int64_t n, void* stream);
  *   rcp_p2p_signal: publish *epoch to each flag_dst[p] (DEVICE array; this
  *                   rank's flag slot in peer p's buffer), release, system scope;
  *   rcp_p2p_wait:   wait until flags[0..n) (this rank's own slots) all reach
- *                   *epoch, acquire; after ~9 s sets *timed_out = 1 and returns
- *                   (the caller checks it) instead of hanging. */
+ *                   *epoch, acquire; after ~9 s sets *timed_out = 1 and traps
+ *                   (a CUDA error at the caller's next sync) instead of hanging
+ *                   or returning a wrong step. */
 int rcp_p2p_epoch_advance(uint64_t* epoch, void* stream);
 int rcp_p2p_put(void* const* dst, int32_t n, const void* src, size_t bytes, uint64_t* const* flag_dst,
                 uint64_t* epoch, uint32_t* counter, void* stream);

@@ -368,9 +368,10 @@ __global__ void p2p_wait_kernel(const unsigned long long* __restrict__ flags, in
     while (true) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + p) : "memory");
       if (v >= e) break;
-      if (clock64() - t0 > (1ll << 34)) {  // ~9 s: a peer is gone; report instead of hanging
-        atomicExch(timed_out, 1);
-        break;
+      if (clock64() - t0 > (1ll << 34)) {  // ~9 s: a peer is gone — record it and fail loudly
+        atomicExch(timed_out, 1);          // (the trap surfaces as a CUDA error at the next sync)
+        __threadfence_system();
+        __trap();
       }
       __nanosleep(64);
     }
