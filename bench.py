@@ -392,7 +392,12 @@ def run_ours(args, cfg, rank, world, local_rank):
         tens[name] = torch.randn((T, h, D), generator=gen, device=dev, dtype=torch.bfloat16)
 
     comm = TorchRingComm() if world > 1 else _LocalComm(0, 1)
-    ring = RingAttention(comm)
+    if args.fp8_qk:  # opt-in FP8 mode: every step's Q range / K block in e4m3 (NOT the bf16 headline)
+        from paper_2411_01783_b200.ring import Fp8QkAttend
+
+        ring = RingAttention(comm, attend=Fp8QkAttend())
+    else:
+        ring = RingAttention(comm)
     cache = RankKvCache(hkv, D, capacity_tokens=plan.total_query_slots() + 4096, device=dev)
 
     per_seq = {n: [t[seq_off[i]:seq_off[i + 1]] for i in range(K)] for n, t in tens.items()}
@@ -409,16 +414,18 @@ def run_ours(args, cfg, rank, world, local_rank):
     events = []
     timing = {"on": False}
 
+    base_attend = ring.attend  # _cuda_attend, or Fp8QkAttend() under --fp8-qk
+
     def timed_attend(*a, **kw):
         if timing["on"]:
             s = torch.cuda.Event(enable_timing=True)
             e = torch.cuda.Event(enable_timing=True)
             s.record()
-            _cuda_attend(*a, **kw)
+            base_attend(*a, **kw)
             e.record()
             events.append((s, e))
         else:
-            _cuda_attend(*a, **kw)
+            base_attend(*a, **kw)
 
     ring.attend = timed_attend
 
@@ -469,7 +476,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     # ---------------- parity of the timed output (outside the timed region):
     # sampled query rows of the LAST timed step vs the fp64 oracle
     parity = None
-    if args.check:
+    if args.check and args.fp8_qk:
+        parity = {"skipped": "--fp8-qk: the bf16 oracle check does not apply (tests/test_gpu_fp8_attention.py "
+                             "checks the FP8 mode against the oracle on the dequantised Q / K)"}
+    elif args.check:
         from oracle.sampled_check import check_plan_rows, check_rank_rows
 
         rows_n = args.check_rows or {"8b": 32, "405b": 16, "405b-1m": 4}[args.config]
@@ -574,7 +584,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         try:
             with open(tpath) as f:
                 tj = json.load(f)
-            traffic = tj.get(args.config, {}).get(str(world))
+            traffic = None if args.fp8_qk else tj.get(args.config, {}).get(str(world))
         except Exception:
             traffic = None
     cpu = None
@@ -586,11 +596,13 @@ def run_ours(args, cfg, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "e4m3 q/k, bf16 p/v (opt-in FP8 mode, not the bf16 headline)" if args.fp8_qk else "bf16",
         "data": "synthetic",
         "config": workload_config(cfg, world, K),
         "latency_ms": ms, "tflops_per_gpu": value / world,
-        "roofline": {"bound": "tensor", "kernel": "attn_fwd_kernel", "achieved": achieved,
+        "roofline": {"bound": "tensor", "kernel": "attn_fwd_qk8_kernel (+ e4m3 quantisation)" if args.fp8_qk
+                     else "attn_fwd_kernel", "achieved": achieved,
                      "peak": pk["bf16_sus"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_sus"],
                      "peak_kind": f"{pk['src']} sustained bf16 (kernel runs inside a long step)",
                      "frac_of_burst": achieved / pk["bf16"], "traffic": traffic,
@@ -605,6 +617,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    if args.fp8_qk:
+        line["config"]["qk_dtype"] = "e4m3"
     print(json.dumps(line), flush=True)
 
 
@@ -623,6 +637,8 @@ def main():
                     help="no-op, kept for old command lines: e2e returns bf16 O by default (fp32 under e2e.fp32_out)")
     ap.add_argument("--e2e-ranges", type=int, default=None,
                     help="query ranges per request in the e2e loop (default: the library's, one per 8192 slots, <= 16)")
+    ap.add_argument("--fp8-qk", action="store_true",
+                    help="opt-in FP8 mode: the ring's attention with e4m3 Q / K (ring.Fp8QkAttend); not the headline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cfg1", action="store_true",
                     help="skip the whole-cfg1 timing (BASELINE configs[0]: GPU arm ~1 s, reference arm ~20 s)")

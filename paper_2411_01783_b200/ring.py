@@ -499,6 +499,23 @@ def _cuda_attend(q, q_pos, q_seq, k, v, k_pos, k_seq, cfg: GqaConfig, out, lse, 
                 cfg.scale, out, lse, mode, ws)
 
 
+class Fp8QkAttend:
+    """Attention callable for ``RingAttention(comm, attend=Fp8QkAttend())``:
+    every ring step's Q range and received K block are quantised to e4m3 with
+    per-head scales (calibrated per call) and the step runs the FP8-QK kernel
+    (rcp_attn_fwd_qk8) — the opt-in FP8 mode of the CP prefill.  Messages,
+    merges and everything else stay bf16 / fp32; the result is the bf16 ring's
+    on the dequantised Q / K of each step."""
+
+    def __call__(self, q, q_pos, q_seq, k, v, k_pos, k_seq, cfg: GqaConfig, out, lse, mode, ws=None):
+        from .attention import attend_into_qk8, quantize_heads_e4m3
+
+        q8, qs = quantize_heads_e4m3(q)
+        k8, ks = quantize_heads_e4m3(k)
+        attend_into_qk8(q8, qs, (q_pos, q_seq), k8, ks, v, (k_pos, k_seq), cfg.n_query_heads, cfg.n_kv_heads,
+                        cfg.scale, out, lse, mode, ws)
+
+
 def _cuda_merge(o_parts, l_parts, out, lse):
     merge_rows_into(o_parts, l_parts, out, lse)
 

@@ -104,3 +104,46 @@ def test_gqa_attention_fp8_cp_step_shape_vs_oracle():
     assert float(d_o.max()) <= 0.25 and float(d_o.mean()) <= 5e-3, (float(d_o.max()), float(d_o.mean()))
     d_l = (got.lse - ref.lse).abs()
     assert float(d_l.max()) <= 0.25 and float(d_l.mean()) <= 1e-2, (float(d_l.max()), float(d_l.mean()))
+
+
+def test_ring_with_fp8_qk_attend_vs_oracle():
+    """RingAttention(attend=Fp8QkAttend()) — the CP prefill's opt-in FP8 mode —
+    on one rank: the pass-KV prefill of a fused two-sequence batch against the
+    oracle on the per-call quantised-then-dequantised Q / K."""
+    import paper_2411_01783_b200 as rc
+    from paper_2411_01783_b200.kv_cache import RankKvCache
+    from paper_2411_01783_b200.ring import Fp8QkAttend, RingAttention, _LocalComm
+    from paper_2411_01783_b200.sharding import SequenceSpec, materialize_rank_block, plan_full_prefill
+
+    rng = np.random.default_rng(17)
+    hq, hkv = 16, 2
+    cfg = rc.GqaConfig(hq, hkv, 128)
+    lens = [700, 333]
+    bf = lambda a: orc.f32_to_bf16_values(np.asarray(a, np.float32))
+    q = [bf(rng.standard_normal((t, hq, 128))) for t in lens]
+    k = [bf(rng.standard_normal((t, hkv, 128))) for t in lens]
+    v = [bf(rng.standard_normal((t, hkv, 128))) for t in lens]
+    plan = plan_full_prefill([SequenceSpec(i, 0, t) for i, t in enumerate(lens)], 1)
+    dev = lambda a: torch.from_numpy(a).cuda().to(torch.bfloat16)
+    qb = materialize_rank_block(plan, 0, [dev(x) for x in q])
+    kb = materialize_rank_block(plan, 0, [dev(x) for x in k])
+    vb = materialize_rank_block(plan, 0, [dev(x) for x in v])
+    ring = RingAttention(_LocalComm(0, 1), attend=Fp8QkAttend())
+    cache = RankKvCache(hkv, 128, capacity_tokens=4096)
+    got = ring.pass_kv_prefill(plan, cache, qb, kb, vb, cfg)
+    torch.cuda.synchronize()
+    # the oracle: Q block and the KV message's K quantised per call exactly as the kernel saw them
+    qd = qb.data.float().cpu().numpy()
+    kd = kb.data.float().cpu().numpy()  # one rank: the message holds the same rows as the block
+    q_deq = orc.dequantize_e4m3(orc.quantize_e4m3(qd, orc.e4m3_scale(qd, hq)), orc.e4m3_scale(qd, hq))
+    k_deq = orc.dequantize_e4m3(orc.quantize_e4m3(kd, orc.e4m3_scale(kd, hkv)), orc.e4m3_scale(kd, hkv))
+    qpos, qseq = qb.positions.cpu().numpy(), qb.seq_ids.cpu().numpy()
+    kv = kb.valid.cpu().numpy()
+    wo, wl = orc.gqa(orc.Blk(q_deq, qpos, qb.valid.cpu().numpy(), qseq),
+                     orc.Blk(k_deq, kb.positions.cpu().numpy(), kv, kb.seq_ids.cpu().numpy()),
+                     orc.Blk(vb.data.float().cpu().numpy(), kb.positions.cpu().numpy(), kv, kb.seq_ids.cpu().numpy()),
+                     hkv)
+    valid = qb.valid.cpu().numpy()
+    assert np.abs(got.output.data.cpu().numpy()[valid] - wo[valid]).max() <= G.O_TOL
+    assert G.lse_err(got.lse.cpu().numpy()[valid], wl[valid]) <= G.LSE_TOL
+    cache.close()
