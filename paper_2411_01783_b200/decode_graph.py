@@ -191,6 +191,7 @@ class GraphedDecode:
         self.ws = torch.empty(max(int(lib.rcp_decode_workspace_bytes(R, H, self.max_len)), 32),
                               dtype=torch.uint8, device=dev)
         self.peer = _PeerDecodeBuffers(comm, S, H, D, dev) if self.transport == "p2p" else None
+        self._mine_cache = {}
         self.graph = None
         self._arena_ptr = None
         self._segs_at_capture = None
@@ -364,13 +365,31 @@ class GraphedDecode:
                 starts[src * S + j], lens[src * S + j] = c.segment(sid)
         return np.concatenate([rows, starts, lens, pos32, seq32])
 
-    def step(self, q_tok: torch.Tensor, k_tok: torch.Tensor, v_tok: torch.Tensor, positions):
+    def input_buffers(self):
+        """The graph's static (q [slots, Hq, D], k, v [slots, Hkv, D]) inputs: a
+        model that writes this rank's new tokens straight into rows [:m] (in
+        the step's ``plan_decode`` assignment order) calls ``step(None, None,
+        None, positions)`` and saves the three input copies."""
+        return self.q_in, self.k_in, self.v_in
+
+    def _mine(self, it: int):
+        """This rank's (seq_id, batch index) assignments at iteration ``it``
+        (plan_decode's round-robin repeats with period N: cached per it % N)."""
+        key = it % self.n
+        got = self._mine_cache.get(key)
+        if got is None:
+            got = self._mine_cache[key] = plan_decode(self.batch, self.n, it).assignments[self.rank]
+        return got
+
+    def step(self, q_tok: torch.Tensor | None, k_tok: torch.Tensor | None, v_tok: torch.Tensor | None, positions):
+        """One decode step.  ``q_tok`` / ``k_tok`` / ``v_tok``: this rank's new
+        tokens in assignment order, or None when the caller already wrote them
+        into ``input_buffers()``."""
         if self.steps_left <= 0:
             raise RuntimeError("GraphedDecode: max_steps reached; create a new GraphedDecode")
-        plan = plan_decode(self.batch, self.n, self.it)
-        mine = plan.assignments[self.rank]
+        mine = self._mine(self.it)
         m = len(mine)
-        if m:
+        if m and q_tok is not None:
             self.q_in[:m].copy_(q_tok[:m])
             self.k_in[:m].copy_(k_tok[:m])
             self.v_in[:m].copy_(v_tok[:m])

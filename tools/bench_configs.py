@@ -195,10 +195,17 @@ def run_decode(args, rank, world):
                                first_positions=None if args.no_table else pos0, grouped_a2a=not args.separate_a2a,
                                transport=args.transport)
 
+            if args.inplace:  # the model writes its new tokens into the graph's input buffers
+                for dst, src in zip(gd.input_buffers(), (qt, kt, vt)):
+                    m0 = min(dst.shape[0], src.shape[0])
+                    dst[:m0].copy_(src[:m0])
+
             def step():  # noqa: F811 - graphed variant
                 it = gd.it
                 own = plan_decode(batch, world, it).assignments[rank]
                 p = [pos0[sid] + it for sid, _b in own]
+                if args.inplace:
+                    return gd.step(None, None, None, p)
                 return gd.step(qt[: len(own)], kt[: len(own)], vt[: len(own)], p)
 
             reset = lambda: None  # noqa: E731 - appends are part of the measured step
@@ -224,6 +231,7 @@ def run_decode(args, rank, world):
                 "q_transport": "allgather" if (args.gather or args.graph) else "ring",
                 "cuda_graph": bool(args.graph), "device_step_table": bool(args.graph and not args.no_table),
                 "transport": args.transport if (args.graph and world > 1) else None,
+                "inputs": "in place" if (args.graph and args.inplace) else "copied per step",
                 "n_q_heads": hq, "n_kv_heads": hkv, "kv_dtype": args.kv_dtype, "step_ms": ms, "step_ms_back_to_back": b2b,
                 "kv_bytes_per_rank": kv_bytes, "hbm_gbs_effective": kv_bytes / (ms * 1e-3) / 1e9}), flush=True)
         if args.graph:
@@ -253,6 +261,8 @@ def main():
                     help="partial: also time pass-Q with peer-memory partials (no All2All), checked bitwise")
     ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
                     help="decode --graph at N > 1: NCCL collectives or kernel stores into CUDA-IPC peer buffers")
+    ap.add_argument("--inplace", action="store_true",
+                    help="decode --graph: inputs written once into GraphedDecode.input_buffers() (no per-step copies)")
     ap.add_argument("--kv-dtype", choices=["bf16", "e4m3"], default="bf16",
                     help="decode: KV-cache storage (e4m3 = FP8 KV, per-head scales calibrated at prefill)")
     ap.add_argument("--steps", type=int, default=5)
