@@ -180,14 +180,10 @@ __global__ void __launch_bounds__(kDecThreads) decode_mma_kernel(const __grid_co
   const int row0 = b * p.hq + kvh * p.group + hc * kDecMaxGroup;  // first query-head row of this CTA
   const int64_t part_base = static_cast<int64_t>(row0) * p.n_split + split;
 
-  if (n_blocks == 0) {  // empty split: (0, -inf)
-    for (int i = threadIdx.x; i < grp * 128; i += blockDim.x) {
-      const int h = i >> 7;
-      p.part_o[(part_base + static_cast<int64_t>(h) * p.n_split) * 128 + (i & 127)] = 0.f;
-      if ((i & 127) == 0) p.part_lse[part_base + static_cast<int64_t>(h) * p.n_split] = -INFINITY;
-    }
-    return;
-  }
+  // A split past the end of its sequence (or an empty slot of the gathered
+  // batch) writes nothing: the combine reads only the ceil(len / keys_per_cta)
+  // splits that hold keys.
+  if (n_blocks == 0) return;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kDecStages; ++s) {
       mbar_init(&full[s], 1);
@@ -465,8 +461,9 @@ struct CombineRoute {
 };
 
 __global__ void __launch_bounds__(kCombineWarps * 32) decode_combine_kernel(
-    const float* __restrict__ part_o, const float* __restrict__ part_lse, int64_t rows, int n_split,
-    float* __restrict__ o, float* __restrict__ lse, CombineRoute route) {
+    const float* __restrict__ part_o, const float* __restrict__ part_lse, int64_t rows, int n_split_alloc,
+    const int64_t* __restrict__ kv_len, int hq, int keys_per_cta, float* __restrict__ o,
+    float* __restrict__ lse, CombineRoute route) {
   // Two passes instead of an online merge: the row's max split LSE first (one
   // read of n_split floats by the whole CTA), then every warp sums its splits
   // weighted by exp(lse_s - max) — no dependent rescale chain, so each warp
@@ -475,8 +472,12 @@ __global__ void __launch_bounds__(kCombineWarps * 32) decode_combine_kernel(
   __shared__ float s_l[kCombineWarps], s_red[kCombineWarps];
   const int64_t row = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const float4* po = reinterpret_cast<const float4*>(part_o + row * n_split * 128);
-  const float* pl = part_lse + row * n_split;
+  const float4* po = reinterpret_cast<const float4*>(part_o + row * n_split_alloc * 128);
+  const float* pl = part_lse + row * n_split_alloc;
+  // only the splits that hold keys of this row's sequence were written
+  const int64_t len = __ldg(kv_len + row / hq);
+  const int64_t used = (len + keys_per_cta - 1) / keys_per_cta;
+  const int n_split = used < n_split_alloc ? static_cast<int>(used) : n_split_alloc;
   float mx = -INFINITY;
   for (int sp = threadIdx.x; sp < n_split; sp += blockDim.x) mx = fmaxf(mx, __ldg(pl + sp));
   for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
@@ -703,7 +704,7 @@ static int decode_launch(const void* q, const void* k, const void* v, int64_t kv
   RCP_CUDA(cudaGetLastError());
   const int64_t rows = batch * hq;
   decode_combine_kernel<<<static_cast<unsigned>(rows), kCombineWarps * 32, 0, st>>>(
-      prm.part_o, prm.part_lse, rows, n_split, o, lse, route);
+      prm.part_o, prm.part_lse, rows, n_split, kv_len, hq, prm.keys_per_cta, o, lse, route);
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
 }
