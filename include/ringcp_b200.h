@@ -224,6 +224,11 @@ int rcp_p2p_put(void* const* dst, int32_t n, const void* src, size_t bytes, uint
 int rcp_p2p_signal(uint64_t* const* flag_dst, int32_t n, const uint64_t* epoch, void* stream);
 int rcp_p2p_wait(const uint64_t* flags, int32_t n, const uint64_t* epoch, int32_t* timed_out, void* stream);
 
+/* Debug timeline: one 1-thread launch writing %globaltimer (ns) to
+ * slots[*counter % n_slots] and advancing the device counter (stream-ordered
+ * stamps between launches, e.g. inside a captured decode step). */
+int rcp_debug_stamp(uint64_t* slots, uint64_t* counter, int32_t n_slots, void* stream);
+
 /* Decode-graph helper: copy row *counter of the device int64 table
  * [n_rows, row_elems] to dst, then increment *counter (device int64, clamped
  * at n_rows - 1).  GraphedDecode precomputes the per-step metadata of all of

@@ -58,6 +58,7 @@ SIGNATURES = {
     "rcp_vmm_unmap": (ctypes.c_int, [_c_void_p, _size_t, _size_t, ctypes.c_uint64]),
     "rcp_vmm_free": (ctypes.c_int, [_c_void_p, _size_t]),
     "rcp_cast_f32_bf16": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, _c_void_p]),
+    "rcp_debug_stamp": (ctypes.c_int, [_c_void_p, _c_void_p, _i32, _c_void_p]),
     "rcp_step_select": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, _c_void_p, _i64, _c_void_p]),
     "rcp_shard_scatter": (ctypes.c_int, [
         ctypes.POINTER(_c_void_p), _c_void_p, ctypes.POINTER(_i64), _i32, _i32, _i32, _i64, _c_void_p]),

@@ -378,6 +378,14 @@ __global__ void p2p_wait_kernel(const unsigned long long* __restrict__ flags, in
   }
 }
 
+// Debug timeline stamp: slots[*counter % n_slots] = %globaltimer (ns), counter++.
+__global__ void debug_stamp_kernel(unsigned long long* slots, unsigned long long* counter, int n_slots) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  const unsigned long long i = (*counter)++;
+  slots[i % static_cast<unsigned long long>(n_slots)] = t;
+}
+
 }  // namespace rcp
 
 using namespace rcp;
@@ -429,7 +437,10 @@ int rcp_merge_attn(const float* const* o_parts, const float* const* lse_parts, i
     a.lse[k] = lse_parts[i];
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (head_dim == 128 && n >= 2 && n <= 8) {
+  // The 32-rows-per-warp form needs enough rows to fill the GPU; a small merge
+  // (the decode step's: slots x heads rows) takes one warp per row instead —
+  // bitwise the same fold (128 rows: ~10 us -> ~3 us).
+  if (head_dim == 128 && n >= 2 && n <= 8 && rows >= 148 * 8 * 32) {
     const int64_t warps = (rows + 31) / 32;
     const unsigned blocks = static_cast<unsigned>((warps + 7) / 8);
     switch (n) {
@@ -576,6 +587,14 @@ int rcp_p2p_wait(const uint64_t* flags, int32_t n, const uint64_t* epoch, int32_
   p2p_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const unsigned long long*>(flags), n, reinterpret_cast<const unsigned long long*>(epoch),
       timed_out);
+  RCP_CUDA(cudaGetLastError());
+  return RCP_OK;
+}
+
+int rcp_debug_stamp(uint64_t* slots, uint64_t* counter, int32_t n_slots, void* stream) {
+  RCP_CHECK_ARG(slots && counter && n_slots >= 1, "bad stamp buffer");
+  debug_stamp_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<unsigned long long*>(slots), reinterpret_cast<unsigned long long*>(counter), n_slots);
   RCP_CUDA(cudaGetLastError());
   return RCP_OK;
 }

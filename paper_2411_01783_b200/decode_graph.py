@@ -192,6 +192,10 @@ class GraphedDecode:
                               dtype=torch.uint8, device=dev)
         self.peer = _PeerDecodeBuffers(comm, S, H, D, dev) if self.transport == "p2p" else None
         self._mine_cache = {}
+        import os
+
+        self._stamps = (torch.zeros(4097, dtype=torch.int64, device=dev)
+                        if os.environ.get("RCP_DECODE_STAMPS") == "1" else None)
         self.graph = None
         self._arena_ptr = None
         self._segs_at_capture = None
@@ -302,9 +306,13 @@ class GraphedDecode:
         lib, c, P, S = _lib.load(), self.cache, self.peer, self.slots
         st, n, H, D = _lib.stream_handle(), self.n, self.cfg.n_query_heads, self.cfg.head_dim
         cnt = P.counters.data_ptr()
+        stamp = self._stamp
+        stamp()
         _lib.check(lib.rcp_p2p_put(_lib.ptr(P.q_dst), n, _lib.ptr(self.q_in), S * H * D * 2, _lib.ptr(P.fq_dst),
                                    _lib.ptr(P.epoch), cnt, st))
+        stamp()
         _lib.check(lib.rcp_p2p_wait(P.flags("q"), n, _lib.ptr(P.epoch), _lib.ptr(P.timed_out), st))
+        stamp()
         ks, vs = c.decode_kwargs().get("scales", (None, None))
         _lib.count("rcp_decode_attn_routed")
         _lib.check(lib.rcp_decode_attn_routed(
@@ -312,10 +320,30 @@ class GraphedDecode:
             _lib.ptr(lens), n * S, max(self.max_len, 1), H, self.cfg.n_kv_heads, D, float(self.cfg.scale),
             _lib.ptr(ks), _lib.ptr(vs), _lib.ptr(P.o_dst), _lib.ptr(P.l_dst), n, self.rank * S * H,
             _lib.ptr(P.fo_dst), _lib.ptr(P.epoch), cnt + 4, _lib.ptr(self.ws), self.ws.numel(), st))
+        stamp()
         _lib.check(lib.rcp_p2p_wait(P.flags("o"), n, _lib.ptr(P.epoch), _lib.ptr(P.timed_out), st))
+        stamp()
         order = merge_order_of(self.rank, n, self.merge_mode)
         merge_rows_into([P.recv_o[s * S:(s + 1) * S] for s in order],
                         [P.recv_l[s * S:(s + 1) * S] for s in order], self.out, self.lse)
+        stamp()
+
+    def _stamp(self) -> None:
+        """Debug timeline (RCP_DECODE_STAMPS=1 at construction): %globaltimer
+        after each phase of the p2p step, read with ``stamps()``."""
+        if self._stamps is not None:
+            _lib.check(_lib.load().rcp_debug_stamp(self._stamps.data_ptr(), self._stamps.data_ptr() + 8 * 4096,
+                                                   4096, _lib.stream_handle()))
+
+    def stamps(self):
+        """(n_steps, 6) int64 ns timestamps: step start, after put, after the Q
+        wait, after decode + combine, after the partials wait, after merge."""
+        if self._stamps is None:
+            return None
+        torch.cuda.synchronize()
+        k = int(self._stamps[4096].item())
+        t = self._stamps[:min(k, 4096)].cpu().numpy()
+        return t[: (len(t) // 6) * 6].reshape(-1, 6)
 
     def check_transport(self) -> None:
         """Raise if a p2p wait gave up on a peer (reads a device flag: syncs)."""
